@@ -1,0 +1,387 @@
+"""Benchmark of the bitplane any-precision GEMV hot path on B200.
+
+Workload (BASELINE.json configs[1]): the Llama-2-7B decode layer set
+(q/k/v/o 4096x4096, gate/up 11008x4096, down 4096x11008), 8-bit parent
+bitplanes + per-row fp16 centroid tables, batch 1, every child bit-width
+k = 3..8.  One STEP = the 7 GEMVs at each of k = 3..8 (42 launches).
+
+metric/value: whole-job algorithmic HBM GB/s = sum of SURVEY.md section 8(d)
+bytes (R*C*k/8 + R*2^k*2 + C*2 + R*2 per GEMV) / device time (CUDA events,
+max over ranks).  Inputs live in HBM; the weights are rotated over 4 copies
+(4 x 203 MB) so no GEMV finds its planes in the 126 MB L2.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the CPU oracle (oracle/anyprec_oracle.c, a C port of
+the reference engine) on all host cores -- the reference package itself is
+numpy-only and publishes no numbers.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPES = [("q", 4096, 4096), ("k", 4096, 4096), ("v", 4096, 4096), ("o", 4096, 4096),
+          ("gate", 11008, 4096), ("up", 11008, 4096), ("down", 4096, 11008)]
+BITS = [3, 4, 5, 6, 7, 8]
+N_MAX = 8
+N_COPIES = 4
+METRIC = "bitplane GEMV µs & HBM GB/s (% roofline) at k=3..8, Llama-2-7B layer shapes"
+
+
+def alg_bytes(rows: int, cols: int, k: int, m: int = 1) -> int:
+    """SURVEY.md section 8(d) algorithmic bytes of one GEMV."""
+    return rows * cols * k // 8 + rows * (1 << k) * 2 + m * cols * 2 + m * rows * 2
+
+
+def step_bytes(shapes, m: int = 1) -> int:
+    return sum(alg_bytes(r, c, k, m) for k in BITS for _, r, c in shapes)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        mhz, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                mhz.append(float(parts[0]))
+                maxes.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None,
+                "sm_max_mhz": max(maxes) if maxes else None,
+                "reasons": sorted(reasons), "samples": len(mhz)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def make_layer_set(torch, seed: int, rank: int, world: int):
+    """Random-init layer set on the device: codes U[0,256), sorted N(0,1)
+    fp16 tables per k (helpers.random_layer semantics).
+    With world > 1 each rank holds its contiguous row shard."""
+    from paper_2402_10517_b200 import AnyPrecisionLayer, engine
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    preps = []
+    for _, rows, cols in SHAPES:
+        r0, r1 = rows * rank // world, rows * (rank + 1) // world
+        codes = torch.randint(0, 256, (r1 - r0, cols), dtype=torch.uint8, device="cuda",
+                              generator=g)
+        tables = {k: torch.sort(torch.randn(r1 - r0, 1 << k, device="cuda", generator=g),
+                                dim=1).values.half() for k in range(3, 9)}
+        layer = AnyPrecisionLayer(n_min=3, n_max=N_MAX, codes=codes, centroid_tables=tables,
+                                  shape=(r1 - r0, cols))
+        preps.append(engine.prepare(layer))
+        del codes
+    return preps
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_10517_b200 import plan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peak, peak_kind = peaks()
+
+    copies = [make_layer_set(torch, 1234 + c, rank, world) for c in range(N_COPIES)]
+    # one plan per (k, layer, copy): per-GEMV launches, copy rotated per launch
+    plans = []
+    i = 0
+    for k in BITS:
+        for li in range(len(SHAPES)):
+            p = plan.GemvPlan([copies[i % N_COPIES][li]], k, m=1, grouped=False)
+            p.x[0][:, : SHAPES[li][2]].normal_()
+            plans.append((k, li, p))
+            i += 1
+    gathers = []
+    if world > 1:
+        for k, li, p in plans:
+            rows = SHAPES[li][1]
+            full = torch.empty((world, -(-rows // world)), dtype=torch.float32, device="cuda")
+            gathers.append(full)
+
+    def step():
+        for j, (k, li, p) in enumerate(plans):
+            p.run()
+            if world > 1:
+                y = p.y[0][0]
+                pad = torch.nn.functional.pad(y, (0, gathers[j].shape[1] - y.shape[0]))
+                dist.all_gather_into_tensor(gathers[j], pad)
+
+    # warm-up (also configures kernel attributes before capture)
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    graph = None
+    if world == 1:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+
+    # per-launch durations (separate pass, events per launch) for the detail table
+    per = {}
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in plans]
+    for _ in range(3):
+        for (k, li, p), (a, b) in zip(plans, ev):
+            a.record()
+            p.run()
+            b.record()
+        torch.cuda.synchronize()
+        for (k, li, p), (a, b) in zip(plans, ev):
+            per.setdefault((k, li), []).append(a.elapsed_time(b) * 1e3)
+
+    # ---- timed region ------------------------------------------------------
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record()
+        for _ in range(args.steps):
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
+        end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clocks = clk.summary()
+
+    full_step_bytes = step_bytes([(n, r, c) for n, r, c in SHAPES])
+    ms_per_step = ms / args.steps
+    value = full_step_bytes / (ms_per_step * 1e-3) / 1e9
+    launches = len(plans) * args.steps
+
+    # grouped launch (all 7 layers of one k in one kernel), for reference
+    gp = [plan.GemvPlan(copies[c], k, m=1, grouped=True) for c in range(N_COPIES) for k in BITS]
+    for p in gp:
+        p.run()
+    torch.cuda.synchronize()
+    gs, ge = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    gs.record()
+    for _ in range(reps):
+        for p in gp:
+            p.run()
+    ge.record()
+    torch.cuda.synchronize()
+    grouped_gbs = sum(p.algorithmic_bytes() for p in gp) * reps / (gs.elapsed_time(ge) * 1e-3) / 1e9
+
+    detail = {}
+    for k in BITS:
+        for li, (name, rows, cols) in enumerate(SHAPES):
+            us = statistics.median(per[(k, li)])
+            b = alg_bytes(rows, cols, k)
+            detail.setdefault(f"k{k}", {})[f"{name}_{rows}x{cols}"] = {
+                "us": round(us, 3), "GBps": round(b / (us * 1e-6) / 1e9, 1)}
+
+    result = {
+        "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f16 x f16 -> f32 accumulate (u8 bitplanes)", "data": "synthetic random-init",
+        "config": {"workload": "llama2-7b decode layer set, 1 B200" if world == 1 else
+                   f"llama2-7b decode layer set, row-sharded over {world} B200 + NCCL all-gather",
+                   "shapes": [f"{n}:{r}x{c}" for n, r, c in SHAPES], "bits": BITS, "batch": 1,
+                   "n_max": N_MAX, "launches_per_step": len(plans), "cuda_graph": graph is not None,
+                   "l2": f"weights rotated over {N_COPIES} copies per launch (inputs > 2x L2)"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": round(value, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(value / peak, 4), "peak_kind": peak_kind, "traffic": None},
+        "clocks": clocks,
+        "grouped_GBps": round(grouped_gbs, 1),
+        "per_gemv": detail,
+    }
+    if rank == 0:
+        result["e2e"] = run_e2e(torch, copies[0])
+        result["cpu_baseline"] = cpu_baseline(sample="one")
+        print(json.dumps(result))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(torch, preps, steps: int = 5):
+    """Same metric through the public drop-in API with host buffers:
+    engine.gemv(prep, x_host_pinned_fp16) -> host y, per GEMV, k = 3..8."""
+    from paper_2402_10517_b200 import engine
+
+    xs = [torch.randn(c, dtype=torch.float16).pin_memory() for _, _, c in SHAPES]
+    h2d = sum(x.numel() * 2 for x in xs) * len(BITS)
+    d2h = sum(r * 4 for _, r, _ in SHAPES) * len(BITS)
+    for k in BITS:  # warm-up
+        for p, x in zip(preps, xs):
+            engine.gemv(p, x, engine.GemvConfig(bit_width=k, activations_fp16=True))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        for k in BITS:
+            for p, x in zip(preps, xs):
+                y = engine.gemv(p, x, engine.GemvConfig(bit_width=k, activations_fp16=True))
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    assert not y.is_cuda
+    return {"value": round(step_bytes(SHAPES) / dt / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": round(dt * 1e3, 3), "api": "engine.gemv(host pinned fp16 x) -> host y"}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference arm / cpu_baseline)
+
+def _oracle_layer_set(seed: int, shapes):
+    from oracle import oracle as ora
+
+    rng = np.random.default_rng(seed)
+    out = []
+    for _, rows, cols in shapes:
+        codes = rng.integers(0, 256, size=(rows, cols), dtype=np.uint8)
+        tables = {k: np.sort(rng.normal(size=(rows, 1 << k)), axis=1).astype(np.float16)
+                  for k in BITS}
+        planes = ora.permute(ora.pack_bitplanes(codes, N_MAX))
+        x = rng.standard_normal(cols).astype(np.float16).astype(np.float32)
+        out.append((planes, cols, tables, x))
+    return out
+
+
+def _oracle_step(ls, threads: int):
+    from oracle import oracle as ora
+
+    for k in BITS:
+        for planes, cols, tables, x in ls:
+            ora.gemm(planes, cols, k, tables[k], x, nthreads=threads)
+
+
+def cpu_baseline(sample: str = "one"):
+    """The oracle C port timed on the host: 1 thread, one full step (the
+    7-layer set at k = 3..8) -- about 10-30 s of CPU work."""
+    ls = _oracle_layer_set(99, SHAPES)
+    t0 = time.perf_counter()
+    _oracle_step(ls, 1)
+    dt = time.perf_counter() - t0
+    return {"value": round(step_bytes(SHAPES) / dt / 1e9, 4), "unit": "GB/s", "cores": 1,
+            "kind": "port", "sample": "one full step (7 layers x k=3..8), 1 thread, "
+            "oracle/anyprec_oracle.c", "seconds": round(dt, 2)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    ls = _oracle_layer_set(99, SHAPES)
+    for _ in range(min(args.warmup, 1)):
+        _oracle_step(ls, threads)
+    steps = max(1, min(args.steps, 3))  # bounded: each step is seconds of CPU work
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        _oracle_step(ls, threads)
+    dt = (time.perf_counter() - t0) / steps
+    v = round(step_bytes(SHAPES) / dt / 1e9, 4)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32 (fp16 tables, fp32 accumulate)", "data": "synthetic random-init",
+        "config": {"workload": "llama2-7b decode layer set", "bits": BITS, "batch": 1},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{steps} full step(s), {threads} threads, oracle/anyprec_oracle.c "
+                                   "(C port of the reference engine.py pipeline)"},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

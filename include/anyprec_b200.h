@@ -1,0 +1,123 @@
+/*
+ * anyprec_b200.h -- C ABI of the B200-native bitplane any-precision hot path.
+ *
+ * Drop-in boundary for the reference package anyprec 0.1.0.  The reference has
+ * no FFI: its "operator API" is the module-level Python functions of
+ * anyprec.bitplane and anyprec.engine.  Each entry point below replaces one of
+ * them (file:line under /root/reference/pkg/src/anyprec/) and is what a
+ * ctypes / cffi binding added to the reference would call.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers (cudaMalloc / torch CUDA storage) unless
+ *     a parameter name starts with h_.  The library never allocates device
+ *     memory inside a call and keeps no global mutable state besides a one-time
+ *     kernel attribute setup; every call is reentrant from many host threads.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Kernels are launched on it; calls do not synchronise.
+ *   - Planes: uint8 [n_max][rows][padded_cols/8]; plane p holds code bit
+ *     n_max-1-p (MSB first, bitplane.py:76-100); byte b bit i = weight 8b+i;
+ *     padded_cols = ceil(cols/1024)*1024 (bitplane.py:72-73).  "permuted"
+ *     layout applies out[4t+j] = in[32j+t] inside every 128-byte tile
+ *     (bitplane.py:31-37, 121-130) and is what the GEMV reads.
+ *   - Centroid tables: IEEE fp16 bit patterns, uint16 [rows][1<<k], one table
+ *     per bit-width k (quantizer.py:75-119 AnyPrecisionLayer.centroid_tables[k]).
+ *   - Activations: fp16 [m][ldx], ldx % 8 == 0, 16-byte aligned base.
+ *   - Return value: APB_OK or an apb_status error code; validation happens on
+ *     the host before any launch (engine.py:263-281 raise-before-compute).
+ */
+#ifndef ANYPREC_B200_H
+#define ANYPREC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the Python shim maps them onto the reference exception
+ * classes of errors.py:4-35. */
+typedef enum {
+    APB_OK = 0,
+    APB_ERR_SHAPE = 1,      /* ShapeError      (errors.py:8-9)   */
+    APB_ERR_PARAM = 2,      /* ParameterError  (errors.py:12-13) */
+    APB_ERR_LAYOUT = 3,     /* LayoutError     (errors.py:20-21) */
+    APB_ERR_CODE_RANGE = 4, /* CodeRangeError  (errors.py:16-17) */
+    APB_ERR_CUDA = 5,       /* CUDA launch / runtime failure    */
+    APB_ERR_NCCL = 6        /* reserved for the collective path */
+} apb_status;
+
+enum { APB_DTYPE_F32 = 0, APB_DTYPE_F16 = 1 };
+
+/* Library version (major*10000 + minor*100 + patch) and status strings. */
+int apb_version(void);
+const char* apb_status_string(int status);
+
+/* bitplane.py:72-73 pad_columns. */
+int64_t apb_pad_columns(int64_t cols);
+
+/* bitplane.py:76-100 pack_bitplanes (+ bitplane.py:126-130 permute_layout when
+ * permuted != 0), in one pass.  codes: uint8 [rows][ld_codes]; planes must hold
+ * n_max*rows*padded_cols/8 bytes.  If d_code_or is not NULL it receives (OR=)
+ * the bitwise OR of every code so the caller can raise CodeRangeError
+ * (bitplane.py:88-91) with one 4-byte read; it must be zeroed by the caller. */
+int apb_pack(const uint8_t* codes, int64_t rows, int64_t cols, int64_t ld_codes, int n_max,
+             int permuted, uint8_t* planes, uint32_t* d_code_or, void* stream);
+
+/* bitplane.py:121-136 permute_layout (inverse=0) / inverse_permute_layout (1).
+ * in and out must not alias. */
+int apb_permute(const uint8_t* in, uint8_t* out, int n_planes, int64_t rows,
+                int64_t padded_cols, int inverse, void* stream);
+
+/* bitplane.py:103-118 unpack_codes: k-bit prefix codes from planes[0..k-1]
+ * only -> uint8 [rows][ld_codes] (cols valid columns per row). */
+int apb_unpack(const uint8_t* planes, int n_max, int64_t rows, int64_t cols,
+               int64_t padded_cols, int permuted, int k, uint8_t* codes, int64_t ld_codes,
+               void* stream);
+
+/* engine.py:75-92 transpose_any_width (k in 2..8) over n word groups:
+ * plane_words uint32 [k][n] (MSB plane first) -> out uint32 [B][n],
+ * B = 2 (k<=2), 4 (k<=4) or 8.  engine.py:48-72 bit_transpose is k = B with
+ * the plane order reversed. */
+int apb_transpose_words(const uint32_t* plane_words, int k, int64_t n, uint32_t* out,
+                        void* stream);
+
+/* engine.py:284-309 gemv and engine.py:312-341 gemm (quantized path).
+ * Reads ONLY planes[0..k-1] (permuted layout) and the k-bit table lut
+ * (uint16 fp16 [rows][1<<k]).
+ *   x      : fp16 [m_x][ldx] activations.  With x_split = 1 the m_x rows are
+ *            (hi, lo) pairs of an fp32 activation (x = hi + lo) and the output
+ *            has m_x/2 rows: y[m] = W.(x_hi[m]) + W.(x_lo[m]).
+ *   y      : [m_out][ldy] of y_dtype (APB_DTYPE_F32 or APB_DTYPE_F16).
+ * Accumulation is fp32 in a fixed order; results are bit-reproducible for
+ * identical inputs and independent of planes k..n_max-1 (test_engine.py:165-176). */
+int apb_gemv(const uint8_t* planes, int n_max, int64_t rows, int64_t cols, int64_t padded_cols,
+             int k, const uint16_t* lut, const uint16_t* x, int m_x, int64_t ldx, int x_split,
+             void* y, int y_dtype, int64_t ldy, void* stream);
+
+/* Grouped form of apb_gemv: n_problems independent layers (same k, m_x,
+ * x_split, y_dtype) in ONE launch, e.g. the seven linears of a decoder block.
+ * Arrays of per-problem pointers/shapes live in HOST memory. */
+int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, const int* n_max,
+                     const int64_t* rows, const int64_t* cols, const int64_t* padded_cols, int k,
+                     const uint16_t* const* lut, const uint16_t* const* x, int m_x,
+                     const int64_t* ldx, int x_split, void* const* y, int y_dtype,
+                     const int64_t* ldy, void* stream);
+
+/* engine.py:357-362 dequantize, from the top-k planes: w [rows][ldw] of
+ * w_dtype (fp16 is exact: the values ARE fp16 table entries). */
+int apb_dequant(const uint8_t* planes, int n_max, int64_t rows, int64_t cols,
+                int64_t padded_cols, int permuted, int k, const uint16_t* lut, void* w,
+                int w_dtype, int64_t ldw, void* stream);
+
+/* Helper for the fp32-activation path: x fp32 [m][ldx_in] -> fp16 pairs
+ * out [2m][ldx_out] with out[2i] = fp16(x[i]), out[2i+1] = fp16(x[i]-out[2i]).
+ * Columns cols..ldx_out-1 are zero-filled.  With round_only = 1 it writes
+ * m rows fp16(x[i]) only (activations_fp16, engine.py:276-277). */
+int apb_split_x(const float* x, int m, int64_t cols, int64_t ldx_in, uint16_t* out,
+                int64_t ldx_out, int round_only, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ANYPREC_B200_H */

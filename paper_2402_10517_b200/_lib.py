@@ -1,0 +1,111 @@
+"""ctypes binding of the C ABI (include/anyprec_b200.h -> libanyprec_b200.so).
+
+The shared library is built in-tree (``make`` or ``__graft_entry__.build()``).
+There is no fallback: if the library is missing or no CUDA device is present
+the calls raise, they never route to a CPU implementation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import (
+    CodeRangeError,
+    DeviceError,
+    LayoutError,
+    ParameterError,
+    ShapeError,
+)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libanyprec_b200.so")
+
+APB_OK = 0
+APB_ERR_SHAPE = 1
+APB_ERR_PARAM = 2
+APB_ERR_LAYOUT = 3
+APB_ERR_CODE_RANGE = 4
+APB_ERR_CUDA = 5
+APB_ERR_NCCL = 6
+APB_DTYPE_F32 = 0
+APB_DTYPE_F16 = 1
+
+# Every symbol declared in include/anyprec_b200.h, with its ctypes signature.
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_PP = ctypes.POINTER(ctypes.c_void_p)
+_PI = ctypes.POINTER(ctypes.c_int)
+_PI64 = ctypes.POINTER(ctypes.c_int64)
+SIGNATURES = {
+    "apb_version": ([], _I),
+    "apb_status_string": ([_I], ctypes.c_char_p),
+    "apb_pad_columns": ([_I64], _I64),
+    "apb_pack": ([_P, _I64, _I64, _I64, _I, _I, _P, _P, _P], _I),
+    "apb_permute": ([_P, _P, _I, _I64, _I64, _I, _P], _I),
+    "apb_unpack": ([_P, _I, _I64, _I64, _I64, _I, _I, _P, _I64, _P], _I),
+    "apb_transpose_words": ([_P, _I, _I64, _P, _P], _I),
+    "apb_gemv": ([_P, _I, _I64, _I64, _I64, _I, _P, _P, _I, _I64, _I, _P, _I, _I64, _P], _I),
+    "apb_gemv_grouped": (
+        [_I, _PP, _PI, _PI64, _PI64, _PI64, _I, _PP, _PP, _I, _PI64, _I, _PP, _I, _PI64, _P],
+        _I,
+    ),
+    "apb_dequant": ([_P, _I, _I64, _I64, _I64, _I, _I, _P, _P, _I, _I64, _P], _I),
+    "apb_split_x": ([_P, _I, _I64, _I64, _P, _I64, _I, _P], _I),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load():
+    """Load the in-tree C-ABI library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise DeviceError(
+                    f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
+                    "there is no CPU fallback"
+                )
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (argtypes, restype) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.argtypes = argtypes
+                fn.restype = restype
+            _lib = lib
+    return _lib
+
+
+_STATUS_EXC = {
+    APB_ERR_SHAPE: ShapeError,
+    APB_ERR_PARAM: ParameterError,
+    APB_ERR_LAYOUT: LayoutError,
+    APB_ERR_CODE_RANGE: CodeRangeError,
+    APB_ERR_CUDA: DeviceError,
+    APB_ERR_NCCL: DeviceError,
+}
+
+
+def check(rc: int, what: str) -> None:
+    if rc == APB_OK:
+        return
+    exc = _STATUS_EXC.get(rc, DeviceError)
+    msg = load().apb_status_string(rc).decode()
+    raise exc(f"{what}: {msg} (status {rc})")
+
+
+def int64_array(vals):
+    return (ctypes.c_int64 * len(vals))(*vals)
+
+
+def int_array(vals):
+    return (ctypes.c_int * len(vals))(*vals)
+
+
+def ptr_array(vals):
+    return (ctypes.c_void_p * len(vals))(*vals)

@@ -1,0 +1,454 @@
+"""GPU parity of the B200 kernels against the reference (golden vectors) and the
+CPU oracle, called through the drop-in API / C ABI.
+
+Bars (see DESIGN.md section "Parity"):
+  * packing, permutation, prefix unpack, SWAR transpose, merged index stream:
+    bit-exact;
+  * gemv / gemm: rel_err (helpers.py:131-137 normwise) < 1e-5 against the
+    reference's fp32 output -- the reference's own oracle tolerance
+    (test_engine.py:149-156); north_star allows 1e-2;
+  * plane isolation, determinism, thread-safety: bit-exact.
+Mirrors test_bitplane.py, test_engine.py and test_acceptance.py #5-#9.
+"""
+
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from oracle import oracle as ora
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2402_10517_b200 import AnyPrecisionLayer, bitplane, engine, errors
+
+    return AnyPrecisionLayer, bitplane, engine, errors
+
+
+@pytest.fixture(scope="module")
+def bp():
+    return np.load(os.path.join(GOLD, "bitplane_golden.npz"))
+
+
+@pytest.fixture(scope="module")
+def tr():
+    return np.load(os.path.join(GOLD, "transpose_golden.npz"))
+
+
+@pytest.fixture(scope="module")
+def eg():
+    return np.load(os.path.join(GOLD, "engine_golden.npz"))
+
+
+def _names(npz, suffix):
+    return sorted({k.split("/")[0] for k in npz.files if k.endswith(suffix)})
+
+
+def _layer_from_golden(api, eg, name):
+    AnyPrecisionLayer = api[0]
+    rows, cols, n_min, n_max = (int(v) for v in eg[f"{name}/meta"])
+    tables = {k: eg[f"{name}/table{k}"] for k in range(n_min, n_max + 1)}
+    return AnyPrecisionLayer(n_min=n_min, n_max=n_max, codes=eg[f"{name}/codes"],
+                             centroid_tables=tables, shape=(rows, cols))
+
+
+def _random_layer(api, seed, rows, cols, n_min=3, n_max=8):
+    AnyPrecisionLayer = api[0]
+    codes, tables = ora.random_layer_arrays(np.random.default_rng(seed), rows, cols, n_min, n_max)
+    return AnyPrecisionLayer(n_min=n_min, n_max=n_max, codes=codes, centroid_tables=tables,
+                             shape=(rows, cols))
+
+
+# ---- bitplane codec (bitplane.py:76-152) ------------------------------------------
+
+def test_pack_permute_unpack_golden(api, bp):
+    _, bitplane, _, _ = api
+    for name in _names(bp, "/linear"):
+        codes = bp[f"{name}/codes"]
+        n_max = int(bp[f"{name}/n_max"])
+        lin = bitplane.pack_bitplanes(codes, n_max)
+        assert lin.layout == "linear" and lin.padded_cols == int(bp[f"{name}/padded"])
+        assert np.array_equal(lin.planes, bp[f"{name}/linear"]), name
+        per = bitplane.permute_layout(lin)
+        assert np.array_equal(per.planes, bp[f"{name}/permuted"]), name
+        fused = bitplane.pack_permuted(codes, n_max)
+        assert np.array_equal(fused.planes.cpu().numpy(), bp[f"{name}/permuted"]), name
+        back = bitplane.inverse_permute_layout(per)
+        assert np.array_equal(back.planes, lin.planes)
+        for k in range(1, n_max + 1):
+            want = bp[f"{name}/unpack{k}"]
+            assert np.array_equal(bitplane.unpack_codes(per, k), want), (name, k)
+            assert np.array_equal(bitplane.unpack_codes(lin, k), want), (name, k)
+
+
+def test_pack_large_matches_oracle(api):
+    _, bitplane, _, _ = api
+    rng = np.random.default_rng(123)
+    for rows, cols, n_max in ((4096, 4096, 8), (37, 11008, 8), (300, 1500, 5)):
+        codes = rng.integers(0, 1 << n_max, size=(rows, cols), dtype=np.uint8)
+        want_lin = ora.pack_bitplanes(codes, n_max)
+        got = bitplane.pack_permuted(codes, n_max).planes.cpu().numpy()
+        assert np.array_equal(got, ora.permute(want_lin)), (rows, cols)
+        assert np.array_equal(bitplane.pack_bitplanes(codes, n_max).planes, want_lin)
+
+
+def test_pack_errors(api):
+    _, bitplane, _, errors = api
+    with pytest.raises(errors.CodeRangeError):
+        bitplane.pack_bitplanes(np.array([[8]]), 3)
+    with pytest.raises(errors.CodeRangeError):  # only the device OR-flag can see this one
+        bitplane.pack_bitplanes(np.array([[1, 2, 200]], dtype=np.uint8), 7)
+    with pytest.raises(errors.ShapeError):
+        bitplane.pack_bitplanes(np.zeros((0, 4), dtype=np.uint8), 3)
+    with pytest.raises(errors.ParameterError):
+        bitplane.pack_bitplanes(np.zeros((2, 4), dtype=np.uint8), 9)
+    t = bitplane.pack_bitplanes(np.array([[1]], dtype=np.uint8), 2)
+    with pytest.raises(errors.ParameterError):
+        bitplane.unpack_codes(t, 0)
+    with pytest.raises(errors.LayoutError):
+        bitplane.inverse_permute_layout(t)
+    with pytest.raises(errors.LayoutError):
+        bitplane.permute_layout(bitplane.permute_layout(t))
+
+
+def test_plane_isolation_unpack(api):
+    # test_bitplane.py:69-79 on the device
+    _, bitplane, _, _ = api
+    rng = np.random.default_rng(4)
+    codes = rng.integers(0, 256, size=(33, 3000), dtype=np.uint8)
+    t = bitplane.pack_permuted(codes, 8)
+    import torch
+
+    for k in range(1, 8):
+        want = bitplane.unpack_codes(t, k).clone()
+        noisy = bitplane.BitplaneTensor(t.planes.clone(), t.rows, t.cols, t.padded_cols, t.layout)
+        noisy.planes[k:] = torch.randint(0, 256, noisy.planes[k:].shape, dtype=torch.uint8,
+                                         device="cuda")
+        assert torch.equal(bitplane.unpack_codes(noisy, k), want), k
+        assert np.array_equal(want.cpu().numpy(), codes >> (8 - k))
+
+
+# ---- SWAR transpose (engine.py:48-92), acceptance #7 --------------------------------
+
+def test_transpose_golden(api, tr):
+    _, _, engine, _ = api
+    for b in (2, 4, 8):
+        assert np.array_equal(engine.bit_transpose(tr[f"bt{b}/in"]), tr[f"bt{b}/out"]), b
+    for k in range(2, 9):
+        assert np.array_equal(engine.transpose_any_width(tr[f"taw{k}/in"], k), tr[f"taw{k}/out"])
+
+
+def test_transpose_million_groups_vs_naive(api):
+    _, _, engine, _ = api
+    rng = np.random.default_rng(555)
+    groups = 1_000_000
+    for k in (2, 3, 4, 5, 6, 7, 8):
+        words = rng.integers(0, 2**32, size=(k, groups), dtype=np.uint32)
+        tw = engine.transpose_any_width(words, k)
+        b = tw.shape[0]
+        mask = np.uint32((1 << b) - 1)
+        # naive per-bit oracle (helpers.py:91-105), vectorised over groups
+        for j in range(32):
+            want = np.zeros(groups, dtype=np.int64)
+            for p in range(k):
+                want |= ((words[p] >> np.uint32(j)) & np.uint32(1)).astype(np.int64) << (k - 1 - p)
+            got = (tw[j % b] >> np.uint32(b * (j // b))) & mask
+            assert np.array_equal(got.astype(np.int64), want), (k, j)
+
+
+def test_transpose_errors(api):
+    _, _, engine, errors = api
+    with pytest.raises(errors.ParameterError):
+        engine.bit_transpose(np.zeros((3, 2), dtype=np.uint32))
+    with pytest.raises(errors.ParameterError):
+        engine.transpose_any_width(np.zeros((1, 4), dtype=np.uint32), 1)
+    with pytest.raises(errors.ShapeError):
+        engine.transpose_any_width(np.zeros((4, 4), dtype=np.uint32), 3)
+
+
+def test_merged_index_stream_golden(api, eg):
+    _, _, engine, _ = api
+    n = 0
+    for name in _names(eg, "/merged_stream"):
+        prep = engine.prepare(_layer_from_golden(api, eg, name))
+        assert np.array_equal(engine._merged_index_stream(prep), eg[f"{name}/merged_stream"]), name
+        n += 1
+    assert n >= 3
+
+
+# ---- GEMV / GEMM (engine.py:284-362), acceptance #5 ------------------------------
+
+def test_gemv_golden_every_k(api, eg):
+    _, _, engine, _ = api
+    for name in _names(eg, "/meta"):
+        layer = _layer_from_golden(api, eg, name)
+        prep = engine.prepare(layer)
+        assert np.array_equal(prep.planes.cpu().numpy(), eg[f"{name}/permuted"]), name
+        x = eg[f"{name}/x"].astype(np.float64)
+        for k in layer.supported_bits():
+            rep = engine.ExecutionReport()
+            y = engine.gemv(prep, x, engine.GemvConfig(bit_width=k), report=rep)
+            assert y.dtype == np.float32 and y.shape == (layer.shape[0],)
+            assert ora.rel_err(y, eg[f"{name}/gemv{k}"]) < TOL, (name, k, ora.rel_err(y, eg[f"{name}/gemv{k}"]))
+            assert [rep.planes_bytes_read, rep.table_bytes_read] == list(eg[f"{name}/gemv{k}/counters"])
+            assert rep.path_taken == str(eg[f"{name}/gemv{k}/path"])
+            y16 = engine.gemv(prep, x, engine.GemvConfig(bit_width=k, activations_fp16=True))
+            assert ora.rel_err(y16, eg[f"{name}/gemv16_{k}"]) < TOL, (name, k)
+
+
+def test_gemm_golden_quantized_and_dense(api, eg):
+    _, _, engine, _ = api
+    for name in _names(eg, "/meta"):
+        layer = _layer_from_golden(api, eg, name)
+        prep = engine.prepare(layer)
+        X = eg[f"{name}/X"]
+        for k in layer.supported_bits():
+            for m in (1, 2, 8, 16, 17):
+                rep = engine.ExecutionReport()
+                y = engine.gemm(prep, X[:m], engine.GemvConfig(bit_width=k), report=rep)
+                want = eg[f"{name}/gemm{k}_m{m}"]
+                assert y.shape == want.shape
+                assert ora.rel_err(y, want) < TOL, (name, k, m, ora.rel_err(y, want))
+                assert rep.path_taken == str(eg[f"{name}/gemm{k}_m{m}/path"]), (name, m)
+                assert [rep.planes_bytes_read, rep.table_bytes_read] == list(
+                    eg[f"{name}/gemm{k}_m{m}/counters"])
+
+
+def test_dequantize_golden(api, eg):
+    _, _, engine, _ = api
+    n = 0
+    for name in _names(eg, "/meta"):
+        layer = _layer_from_golden(api, eg, name)
+        for k in layer.supported_bits():
+            key = f"{name}/dequant{k}"
+            if key in eg.files:
+                assert np.array_equal(engine.dequantize(layer, k), eg[key]), (name, k)
+                n += 1
+    assert n > 10
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096), (11008, 4096), (4096, 11008)])
+def test_gemv_llama7b_shapes_vs_oracle(api, shape):
+    _, _, engine, _ = api
+    rows, cols = shape
+    layer = _random_layer(api, 7 + rows + cols, rows, cols)
+    prep = engine.prepare(layer)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(cols)
+    per = prep.planes.cpu().numpy()
+    for k in range(3, 9):
+        t = layer.centroid_tables[k]
+        want = ora.gemm(per, cols, k, t, ora.prep_x(x, cols, False), nthreads=8)
+        y = engine.gemv(prep, x, engine.GemvConfig(bit_width=k))
+        assert ora.rel_err(y, want) < TOL, (shape, k, ora.rel_err(y, want))
+        want16 = ora.gemm(per, cols, k, t, ora.prep_x(x, cols, True), nthreads=8)
+        y16 = engine.gemv(prep, x, engine.GemvConfig(bit_width=k, activations_fp16=True))
+        assert ora.rel_err(y16, want16) < TOL, (shape, k)
+
+
+@pytest.mark.parametrize("m", [1, 2, 4, 8, 16, 40])
+def test_small_batch_gemm_vs_oracle(api, m):
+    _, _, engine, _ = api
+    rows, cols = 333, 2500  # ragged rows and columns
+    layer = _random_layer(api, 50 + m, rows, cols, 2, 8)
+    prep = engine.prepare(layer)
+    X = np.random.default_rng(m).standard_normal((m, cols))
+    per = prep.planes.cpu().numpy()
+    for k in (2, 3, 4, 5, 8):
+        t = layer.centroid_tables[k]
+        cfg = engine.GemvConfig(bit_width=k, dense_threshold=64)
+        rep = engine.ExecutionReport()
+        y = engine.gemm(prep, X, cfg, report=rep)
+        assert rep.path_taken == "gemm-quantized"
+        want = ora.gemm(per, cols, k, t, ora.prep_x(X, cols, False), nthreads=8)
+        assert ora.rel_err(y, want) < TOL, (m, k, ora.rel_err(y, want))
+        y16 = engine.gemm(prep, X, engine.GemvConfig(bit_width=k, dense_threshold=64,
+                                                     activations_fp16=True))
+        want16 = ora.gemm(per, cols, k, t, ora.prep_x(X, cols, True), nthreads=8)
+        assert ora.rel_err(y16, want16) < TOL, (m, k)
+
+
+def test_acceptance_corpus_vs_dense_oracle(api):
+    # test_acceptance.py:136-174 corpus: 50 layers up to 4096x4096, gemv vs the
+    # fp64 dense oracle at every supported k.
+    _, _, engine, _ = api
+    rng = np.random.default_rng(4242)
+    sizes = [(4096, 4096), (2048, 2048)]
+    for _ in range(12):
+        sizes.append((int(rng.integers(64, 257)), int(rng.integers(512, 2049))))
+    while len(sizes) < 50:
+        sizes.append((int(rng.integers(2, 64)), int(rng.integers(8, 513))))
+    for rows, cols in sizes:
+        n_min = int(rng.integers(2, 5))
+        n_max = int(rng.integers(n_min, 9))
+        AnyPrecisionLayer = api[0]
+        codes, tables = ora.random_layer_arrays(rng, rows, cols, n_min, n_max)
+        layer = AnyPrecisionLayer(n_min=n_min, n_max=n_max, codes=codes, centroid_tables=tables,
+                                  shape=(rows, cols))
+        prep = engine.prepare(layer)
+        x = rng.normal(size=cols)
+        for k in layer.supported_bits():
+            y = engine.gemv(prep, x, engine.GemvConfig(bit_width=k))
+            ref = ora.dense_reference_gemv(codes, n_max, tables[k], x, k)
+            assert ora.rel_err(y, ref) < TOL, (rows, cols, k, ora.rel_err(y, ref))
+
+
+def test_plane_isolation_gemv_bit_exact(api):
+    # test_engine.py:165-176 / acceptance #6: corrupting planes >= k leaves y identical
+    import torch
+
+    _, _, engine, _ = api
+    layer = _random_layer(api, 6, 100, 3100, 2, 8)
+    prep = engine.prepare(layer)
+    x = torch.randn(3100, device="cuda")
+    for k in range(2, 9):
+        want = engine.gemv(prep, x, engine.GemvConfig(bit_width=k)).clone()
+        noisy = engine.prepare(layer)
+        if k < 8:
+            noisy.planes[k:] = torch.randint(0, 256, noisy.planes[k:].shape, dtype=torch.uint8,
+                                             device="cuda")
+        got = engine.gemv(noisy, x, engine.GemvConfig(bit_width=k))
+        assert torch.equal(got, want), k
+
+
+def test_merged_and_plain_bit_identical(api):
+    _, _, engine, _ = api
+    layer = _random_layer(api, 7, 64, 2048, 3, 5)
+    prep = engine.prepare(layer)
+    x = np.random.default_rng(7).normal(size=2048)
+    a = engine.gemv(prep, x, engine.GemvConfig(bit_width=3, use_merged_table=True))
+    b = engine.gemv(prep, x, engine.GemvConfig(bit_width=3, use_merged_table=False))
+    assert np.array_equal(a, b)
+
+
+def test_deterministic_and_thread_safe(api):
+    # test_engine.py:311-323
+    _, _, engine, _ = api
+    layer = _random_layer(api, 23, 1200, 2048, 2, 6)
+    prep = engine.prepare(layer)
+    rng = np.random.default_rng(23)
+    xs = [rng.normal(size=2048) for _ in range(16)]
+    cfg = engine.GemvConfig(bit_width=4)
+    serial = [engine.gemv(prep, x, cfg) for x in xs]
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        parallel = list(pool.map(lambda x: engine.gemv(prep, x, cfg), xs))
+    for a, b in zip(serial, parallel):
+        assert np.array_equal(a, b)
+    again = [engine.gemv(prep, x, cfg) for x in xs]
+    for a, b in zip(serial, again):
+        assert np.array_equal(a, b)
+
+
+def test_bandwidth_counters_proportional(api):
+    # acceptance #9: planes bytes read scale exactly as k/8
+    _, _, engine, _ = api
+    layer = _random_layer(api, 999, 32, 3000, 2, 8)
+    prep = engine.prepare(layer)
+    x = np.random.default_rng(9).normal(size=3000)
+    reads = {}
+    for k in range(2, 9):
+        rep = engine.ExecutionReport()
+        engine.gemv(prep, x, engine.GemvConfig(bit_width=k), report=rep)
+        reads[k] = rep.planes_bytes_read
+    for k in range(2, 9):
+        assert reads[k] * 8 == reads[8] * k
+
+
+def test_gemv_errors(api):
+    _, _, engine, errors = api
+    layer = _random_layer(api, 11, 2, 1024, 3, 5)
+    prep = engine.prepare(layer)
+    with pytest.raises(errors.ShapeError):
+        engine.gemv(prep, np.zeros(1000), engine.GemvConfig(bit_width=3))
+    with pytest.raises(errors.ParameterError):
+        engine.gemv(prep, np.zeros(1024), engine.GemvConfig(bit_width=2))
+    with pytest.raises(errors.ShapeError):
+        engine.gemv(prep, np.zeros((2, 1024)), engine.GemvConfig(bit_width=3))
+    with pytest.raises(errors.ParameterError):
+        engine.gemv(prep, np.zeros(1024), engine.GemvConfig(bit_width=4, use_merged_table=True))
+    with pytest.raises(errors.ShapeError):
+        engine.gemm(prep, np.zeros((0, 1024)), engine.GemvConfig(bit_width=3))
+    with pytest.raises(errors.ShapeError):
+        engine.gemm(prep, np.zeros(1024), engine.GemvConfig(bit_width=3))
+    with pytest.raises(errors.ShapeError):
+        engine.gemm(prep, np.zeros((64, 1000)), engine.GemvConfig(bit_width=3))
+    with pytest.raises(errors.ParameterError):
+        engine.dequantize(layer, 2)
+
+
+def test_device_tensors_stay_on_device(api):
+    import torch
+
+    _, _, engine, _ = api
+    layer = _random_layer(api, 12, 256, 4096)
+    prep = engine.prepare(layer)
+    x = torch.randn(4096, device="cuda")
+    y = engine.gemv(prep, x, engine.GemvConfig(bit_width=4))
+    assert y.is_cuda and y.dtype == torch.float32
+    yh = engine.gemv(prep, x.cpu().numpy(), engine.GemvConfig(bit_width=4))
+    assert np.array_equal(y.cpu().numpy(), yh)
+    x16 = x.half()
+    y16 = engine.gemv(prep, x16, engine.GemvConfig(bit_width=4))
+    y16b = engine.gemv(prep, x16.float(), engine.GemvConfig(bit_width=4, activations_fp16=True))
+    assert torch.equal(y16, y16b)
+
+
+def test_grouped_equals_single(api):
+    # the grouped launch (one kernel for several layers) is bit-identical
+    import torch
+
+    from paper_2402_10517_b200 import plan
+
+    _, _, engine, _ = api
+    shapes = [(4096, 4096), (1100, 4096), (4096, 11008), (17, 300)]
+    preps = [engine.prepare(_random_layer(api, 100 + i, r, c)) for i, (r, c) in enumerate(shapes)]
+    for k in (3, 4, 6, 8):
+        p = plan.GemvPlan(preps, k, m=1, grouped=True)
+        q = plan.GemvPlan(preps, k, m=1, grouped=False)
+        for xa, xb in zip(p.x, q.x):
+            xb.copy_(xa)
+        p.run()
+        q.run()
+        torch.cuda.synchronize()
+        for ya, yb in zip(p.y, q.y):
+            assert torch.equal(ya, yb), k
+
+
+def test_large_shape_properties(api):
+    # size-independent properties at 70B shapes: (1) GPU unpack == codes >> (8-k)
+    # bit-exact; (2) linearity y(a+b) = y(a) + y(b); (3) checksum of checksums:
+    # sum_r y_r == x . colsum(dequant_k(W)) using the (independent) dequant kernel.
+    import torch
+
+    _, bitplane, engine, _ = api
+    AnyPrecisionLayer = api[0]
+    rows, cols = 28672, 8192
+    g = torch.Generator(device="cuda").manual_seed(0)
+    codes = torch.randint(0, 256, (rows, cols), dtype=torch.uint8, device="cuda", generator=g)
+    tables = {k: torch.sort(torch.randn(rows, 1 << k, device="cuda", generator=g), dim=1).values.half()
+              for k in range(3, 9)}
+    layer = AnyPrecisionLayer(n_min=3, n_max=8, codes=codes, centroid_tables=tables,
+                              shape=(rows, cols))
+    prep = engine.prepare(layer)
+    for k in (3, 5, 8):
+        assert torch.equal(bitplane.unpack_codes(prep.tensor, k), codes >> (8 - k)), k
+    a = torch.randn(cols, device="cuda", generator=g).half()
+    b = torch.randn(cols, device="cuda", generator=g).half()
+    for k in (3, 4, 8):
+        cfg = engine.GemvConfig(bit_width=k)
+        ya, yb = engine.gemv(prep, a, cfg), engine.gemv(prep, b, cfg)
+        yab = engine.gemv(prep, (a.float() + b.float()), cfg)
+        assert ora.rel_err((ya + yb).cpu().numpy(), yab.cpu().numpy()) < TOL, k
+        w = engine.dequantize(prep, k).double()
+        colsum = w.sum(0)
+        lhs = float(ya.double().sum())
+        rhs = float((a.double() * colsum).sum())
+        scale = float((a.double().abs() * w.abs().sum(0)).sum())
+        assert abs(lhs - rhs) <= 1e-5 * scale, (k, lhs, rhs)
