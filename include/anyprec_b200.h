@@ -48,6 +48,13 @@ typedef enum {
 
 enum { APB_DTYPE_F32 = 0, APB_DTYPE_F16 = 1 };
 
+/* apb_gemv* flags.  APB_FLAG_PDL launches with programmatic stream
+ * serialisation: the kernel may start (and read planes / tables) while the
+ * previous kernel in the stream is still running, and waits for it before
+ * reading activations or writing outputs.  Only set it when the preceding
+ * kernel does not write the planes or tables of this call. */
+enum { APB_FLAG_PDL = 1 };
+
 /* Library version (major*10000 + minor*100 + patch) and status strings. */
 int apb_version(void);
 const char* apb_status_string(int status);
@@ -92,7 +99,7 @@ int apb_transpose_words(const uint32_t* plane_words, int k, int64_t n, uint32_t*
  * identical inputs and independent of planes k..n_max-1 (test_engine.py:165-176). */
 int apb_gemv(const uint8_t* planes, int n_max, int64_t rows, int64_t cols, int64_t padded_cols,
              int k, const uint16_t* lut, const uint16_t* x, int m_x, int64_t ldx, int x_split,
-             void* y, int y_dtype, int64_t ldy, void* stream);
+             void* y, int y_dtype, int64_t ldy, int flags, void* stream);
 
 /* Grouped form of apb_gemv: n_problems independent layers (same k, m_x,
  * x_split, y_dtype) in ONE launch, e.g. the seven linears of a decoder block.
@@ -101,7 +108,7 @@ int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, const int* n_
                      const int64_t* rows, const int64_t* cols, const int64_t* padded_cols, int k,
                      const uint16_t* const* lut, const uint16_t* const* x, int m_x,
                      const int64_t* ldx, int x_split, void* const* y, int y_dtype,
-                     const int64_t* ldy, void* stream);
+                     const int64_t* ldy, int flags, void* stream);
 
 /* engine.py:357-362 dequantize, from the top-k planes: w [rows][ldw] of
  * w_dtype (fp16 is exact: the values ARE fp16 table entries). */

@@ -20,7 +20,8 @@ from .errors import (
 )
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libanyprec_b200.so")
+# APB_LIB_PATH overrides the library (tuning / instrumented builds only)
+LIB_PATH = os.environ.get("APB_LIB_PATH") or os.path.join(_HERE, "libanyprec_b200.so")
 
 APB_OK = 0
 APB_ERR_SHAPE = 1
@@ -31,6 +32,7 @@ APB_ERR_CUDA = 5
 APB_ERR_NCCL = 6
 APB_DTYPE_F32 = 0
 APB_DTYPE_F16 = 1
+APB_FLAG_PDL = 1
 
 # Every symbol declared in include/anyprec_b200.h, with its ctypes signature.
 _P = ctypes.c_void_p
@@ -47,9 +49,9 @@ SIGNATURES = {
     "apb_permute": ([_P, _P, _I, _I64, _I64, _I, _P], _I),
     "apb_unpack": ([_P, _I, _I64, _I64, _I64, _I, _I, _P, _I64, _P], _I),
     "apb_transpose_words": ([_P, _I, _I64, _P, _P], _I),
-    "apb_gemv": ([_P, _I, _I64, _I64, _I64, _I, _P, _P, _I, _I64, _I, _P, _I, _I64, _P], _I),
+    "apb_gemv": ([_P, _I, _I64, _I64, _I64, _I, _P, _P, _I, _I64, _I, _P, _I, _I64, _I, _P], _I),
     "apb_gemv_grouped": (
-        [_I, _PP, _PI, _PI64, _PI64, _PI64, _I, _PP, _PP, _I, _PI64, _I, _PP, _I, _PI64, _P],
+        [_I, _PP, _PI, _PI64, _PI64, _PI64, _I, _PP, _PP, _I, _PI64, _I, _PP, _I, _PI64, _I, _P],
         _I,
     ),
     "apb_dequant": ([_P, _I, _I64, _I64, _I64, _I, _I, _P, _P, _I, _I64, _P], _I),

@@ -4,34 +4,37 @@
 // path) of the reference.  Same maths: y[m][r] = sum_c LUT_k[r][code_k(r,c)] *
 // x[m][c], reading ONLY planes 0..k-1 and the k-bit table.
 //
-// CTA  = 16 output rows x all K columns; W warps split the K dimension into
-//        "units" (one 16- or 8-byte slice of a 128-byte tile-plane row per
-//        lane).  Deterministic: every output is reduced in a fixed order
-//        (mma k-order, then warps 0..W-1 through shared memory).
-// Lane = (g, q) = (lane>>2, lane&3): lane owns rows g and g+8 of the CTA and a
-//        fixed set of columns; it loads k plane words per row with 128-bit
-//        (or 64-bit) streaming loads (ld.global.nc.L1::no_allocate).
+// Work item = one 16-row block of one problem (layer) x all K columns.
+// Persistent grid: each CTA owns a contiguous, cost-balanced range of items
+// (possibly spanning several layers of a grouped launch) and streams them:
+// while a row block is being computed, the planes of the next units (which
+// may belong to the next row block) are already in flight in registers and
+// the next block's centroid rows are being copied into shared memory by
+// cp.async, so the per-block prologue (DRAM latency + table build) is hidden.
+//
+// Inside an item, W warps split the K dimension into "units" (one 16- or
+// 8-byte slice of a 128-byte tile-plane row per lane).  Lane (g, q) =
+// (lane>>2, lane&3) owns rows g and g+8 of the block.
 // Decode: bit networks of apb_common.cuh (no per-weight shift/mask):
-//        k <= 4: to_pairs -> one PRMT + one LDS per PAIR of weights from a
-//                4^k-entry pair table (paper's merged lookup)
-//        k >= 5: to_bytes -> one PRMT + one LDS per weight, pairs packed into
-//                fp16x2 with one IMAD (FMA pipe).
-//        Shared-memory tables are replicated per lane slot ([entry][row-half]
-//        [lane]) so every lookup is bank-conflict free (bank == lane), and the
-//        PRMT builds the full byte address [lane*4 | row-half*128 | idx<<8]
-//        in one instruction; the table base folds into the LDS immediate.
-// MAC:   the decoded fp16x2 weights ARE the A fragment of
-//        mma.sync.m16n8k16 (rows g, g+8; k-slots 2q.., 2q+8..), the
-//        activations are the B fragment (batch columns n = g), accumulation is
-//        fp32 in the tensor core.  This offloads the multiply-add (1 HMMA per
-//        256 weights instead of 128 FFMA) from the ALU/FMA pipes, which the
-//        decode saturates on B200, and makes batch 1..8 (or 1..4 with fp32
-//        hi/lo activations) cost the same instructions as batch 1.
+//   k <= 4: to_pairs -> one PRMT + one LDS per PAIR of weights from a 4^k
+//           entry pair table (the paper's merged lookup);
+//   k >= 5: to_bytes -> one PRMT + one LDS per weight, pairs packed into
+//           fp16x2 with one IMAD (FMA pipe).
+//   Tables are replicated per lane slot ([entry][row-half][lane]) so every
+//   lookup is bank-conflict free (bank == lane); one PRMT builds the byte
+//   address [lane*4 | row-half*128 | idx<<8], the table base folds into the
+//   LDS immediate.
+// MAC: the decoded fp16x2 weights ARE the A fragment of mma.sync.m16n8k16
+//   (rows g, g+8; k-slots 2q.., 2q+8..), the activations the B fragment
+//   (batch columns n = g), accumulation fp32 in the tensor core: 1 HMMA per
+//   256 weights instead of 128 FFMA, and batch 1..8 costs the same as batch 1.
+// Deterministic: fixed mma k-order, fixed chain split, warps reduced 0..W-1.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
 
 #include "../../include/anyprec_b200.h"
 #include "apb_common.cuh"
@@ -40,6 +43,27 @@ namespace apb {
 
 constexpr int kMaxGroup = 16;
 constexpr int kRowsPerCta = 16;
+#ifndef APB_WARPS
+#define APB_WARPS 8
+#endif
+constexpr int kWarps = APB_WARPS;
+
+#ifdef APB_TIMELINE
+// Debug builds (tools/timeline): per-CTA phase timestamps (globaltimer, ns).
+__device__ unsigned long long* g_timeline = nullptr;
+#define APB_TS(i)                                                          \
+    do {                                                                   \
+        if (threadIdx.x == 0 && g_timeline) {                              \
+            unsigned long long t_;                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));         \
+            g_timeline[(size_t)blockIdx.x * 8 + (i)] = t_;                 \
+        }                                                                  \
+    } while (0)
+#else
+#define APB_TS(i) \
+    do {          \
+    } while (0)
+#endif
 
 struct GemvProblem {
     const uint8_t* planes;  // permuted planes, plane 0 (MSB) first
@@ -48,15 +72,20 @@ struct GemvProblem {
     void* y;                // [m_out][ldy]
     int64_t rows, cols, row_bytes, plane_stride, ldx, ldy;
     int n_tiles;
-    int block_begin;
+    int item_begin;         // first global item (row block) of this problem
+    int64_t cost_begin;     // prefix cost (tiles) of the items before this problem
 };
 
 struct GemvLaunch {
     GemvProblem prob[kMaxGroup];
     int n_prob;
+    int n_items;
+    int64_t total_cost;
     int m_x;
     int x_split;
     int y_f16;
+    int64_t xs_bytes;  // > 0: activations staged in shared memory ([m_x][padded] fp16)
+    int flags;         // APB_FLAG_*
 };
 
 template <int UB>
@@ -78,9 +107,19 @@ struct UnitVec<8> {
     static __device__ __forceinline__ uint32_t word(const T& v, int i) { return i == 0 ? v.x : v.y; }
 };
 
-__device__ __forceinline__ uint32_t lds32(const uint8_t* base, uint32_t off) {
-    return *reinterpret_cast<const uint32_t*>(base + off);
+// Shared-window address of the dynamic shared memory (the lookup table sits at
+// its start).  sm_100 reserves the first 1 KB of the window, so the table is at
+// 0x400; the kernel verifies this at entry (and traps otherwise) so the table
+// lookup can be a single LDS [R + imm] with the PRMT-built byte offset --
+// without it ptxas keeps the base in a general register and spends one IADD
+// per lookup.
+#define APB_SMEM_BASE 1024
+__device__ __forceinline__ uint32_t lds_table(uint32_t off) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+1024];" : "=r"(v) : "r"(off));
+    return v;
 }
+__device__ __forceinline__ uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
 __device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -91,7 +130,15 @@ __device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uin
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// 8 fp16 activations at columns col..col+7, zero beyond cols (tail tile only).
+// cp.async 16 bytes, zero-filling beyond src_bytes (0..16).
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int src_bytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gsrc), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// 8 fp16 activations at columns col..col+7, zero beyond cols (tail tile, global path).
 __device__ __noinline__ uint4 load_x8_tail(const uint16_t* xrow, int64_t col, int64_t cols) {
     if (col + 8 <= cols) return __ldg(reinterpret_cast<const uint4*>(xrow + col));
     uint32_t h[8];
@@ -110,13 +157,13 @@ struct TableGeom {
     static constexpr bool kPair = K <= 4;
     static constexpr int kEntries = kPair ? (1 << (2 * K)) : (1 << K);
     static constexpr int kBytes = kEntries * 256;  // [entry][row-half 2][lane 32] x u32
+    static constexpr int kStageBytes = kRowsPerCta * (1 << K) * 2;  // 16 centroid rows
 };
 
 // Decode one lane word of one row into 16 fp16x2 values:
 // out[p*4 + j] = weights of columns (256p + 8t + 2j, +1) of this row.
 template <int K>
-__device__ __forceinline__ void decode_word(const uint32_t* Q, const uint8_t* table, uint32_t off,
-                                            uint32_t* out) {
+__device__ __forceinline__ void decode_word(const uint32_t* Q, uint32_t off, uint32_t* out) {
     if constexpr (TableGeom<K>::kPair) {
         uint32_t U[4];
         to_pairs<K>(Q, U);
@@ -124,7 +171,7 @@ __device__ __forceinline__ void decode_word(const uint32_t* Q, const uint8_t* ta
         for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int p = 0; p < 4; ++p)
-                out[p * 4 + j] = lds32(table, prmt(U[j], off, 0x5504u | (uint32_t)(p << 4)));
+                out[p * 4 + j] = lds_table(prmt(U[j], off, 0x5504u | (uint32_t)(p << 4)));
     } else {
         uint32_t Wb[8];
         to_bytes<K>(Q, Wb);
@@ -133,8 +180,8 @@ __device__ __forceinline__ void decode_word(const uint32_t* Q, const uint8_t* ta
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 const uint32_t sel = 0x5504u | (uint32_t)(p << 4);
-                const uint32_t e = lds32(table, prmt(Wb[2 * j], off, sel));
-                const uint32_t o = lds32(table, prmt(Wb[2 * j + 1], off, sel));
+                const uint32_t e = lds_table(prmt(Wb[2 * j], off, sel));
+                const uint32_t o = lds_table(prmt(Wb[2 * j + 1], off, sel));
                 out[p * 4 + j] = e + (o << 16);  // IMAD: o * 65536 + e (e < 65536)
             }
     }
@@ -142,251 +189,445 @@ __device__ __forceinline__ void decode_word(const uint32_t* Q, const uint8_t* ta
 
 template <int NG>
 struct GemvBounds {
-    // NG == 1: up to 12 warps (<= 168 registers); wider batches: 8 warps (<= 255).
-    static constexpr int kThreads = NG == 1 ? 384 : 256;
+    // NG == 1: <= 128 registers so 16 warps (two 256-thread CTAs) are resident per SM.
+    static constexpr int kThreads = kWarps * 32;
+    static constexpr int kMinBlocks = NG == 1 ? 16 / kWarps : 8 / kWarps;
 };
 
-template <int K, int NG, int UB>
-__global__ void __launch_bounds__(GemvBounds<NG>::kThreads) gemv_kernel(const __grid_constant__ GemvLaunch L) {
-    using V = UnitVec<UB>;
-    using VT = typename V::T;
-    constexpr int WPU = UB / 4;             // lane words per unit per row
-    constexpr int UPT = 128 / (4 * UB);     // units per tile
-    constexpr int TB = TableGeom<K>::kBytes;
-
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* table = smem;
-    uint8_t* scratch = smem + TB;
-
+__device__ __forceinline__ int problem_of(const GemvLaunch& L, int item) {
     int pi = 0;
 #pragma unroll 1
     for (int i = 1; i < L.n_prob; ++i)
-        if ((int)blockIdx.x >= L.prob[i].block_begin) pi = i;
-    // problem fields -> registers once (avoid indexed constant-bank reloads in the loop)
-    const uint8_t* const planes = L.prob[pi].planes;
-    const uint16_t* const lut = L.prob[pi].lut;
-    const uint16_t* const xg = L.prob[pi].x;
-    void* const yg = L.prob[pi].y;
-    const int64_t rows = L.prob[pi].rows, cols = L.prob[pi].cols;
-    const int64_t row_bytes = L.prob[pi].row_bytes, plane_stride = L.prob[pi].plane_stride;
-    const int64_t ldx = L.prob[pi].ldx, ldy = L.prob[pi].ldy;
-    const int n_tiles = L.prob[pi].n_tiles;
-    const int64_t rb = (int64_t)blockIdx.x - L.prob[pi].block_begin;
+        if (item >= L.prob[i].item_begin) pi = i;
+    return pi;
+}
+
+// First item whose cumulative cost start is >= target (items are cost-uniform
+// within a problem, cost = n_tiles).  Used to give every CTA a contiguous,
+// cost-balanced item range.
+__device__ __forceinline__ int item_at_cost(const GemvLaunch& L, int64_t target) {
+    if (target >= L.total_cost) return L.n_items;
+#pragma unroll 1
+    for (int i = 0; i < L.n_prob; ++i) {
+        const GemvProblem& P = L.prob[i];
+        const int n = (i + 1 < L.n_prob ? L.prob[i + 1].item_begin : L.n_items) - P.item_begin;
+        const int64_t end = P.cost_begin + (int64_t)n * P.n_tiles;
+        if (target < end) {
+            const int64_t d = target - P.cost_begin;
+            return P.item_begin + (int)((d + P.n_tiles - 1) / P.n_tiles);
+        }
+    }
+    return L.n_items;
+}
+
+template <int K, int NG, int UB, bool XS>
+__global__ void __launch_bounds__(GemvBounds<NG>::kThreads, GemvBounds<NG>::kMinBlocks)
+    gemv_kernel(const __grid_constant__ GemvLaunch L) {
+    using V = UnitVec<UB>;
+    using VT = typename V::T;
+    using TG = TableGeom<K>;
+    constexpr int WPU = UB / 4;          // lane words per unit per row
+    constexpr int UPT = 128 / (4 * UB);  // units per tile
+    constexpr int RC = 8 * NG;           // reduction columns
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* const table = smem;                      // [TB]
+    uint8_t* const stage = smem + TG::kBytes;         // [16 rows][2^K] fp16 (next item)
+    float* const red = reinterpret_cast<float*>(stage + TG::kStageBytes);  // [W][16][RC]
+    uint8_t* const xs = reinterpret_cast<uint8_t*>(red + kWarps * kRowsPerCta * RC);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, q = lane & 3;
-    const int nwarps = blockDim.x >> 5;
-    const int64_t row0 = rb * kRowsPerCta + g, row1 = row0 + 8;
-    const bool ok0 = row0 < rows, ok1 = row1 < rows;
-    const int n_units = n_tiles * UPT;
+    const int nthreads = blockDim.x;
+    if ((uint32_t)__cvta_generic_to_shared(smem) != APB_SMEM_BASE) __trap();  // see lds_table
 
-    auto load_unit = [&](int u, VT (&dst)[2][K]) {
-        const int tile = u / UPT, s = u - tile * UPT;
-        const int64_t off = (int64_t)tile * kTileBytes + s * 4 * UB + q * UB;
-        const uint8_t* b0 = planes + row0 * row_bytes + off;
-        const uint8_t* b1 = planes + row1 * row_bytes + off;
+    // contiguous cost-balanced item range of this CTA
+    const int first = item_at_cost(L, L.total_cost * (int64_t)blockIdx.x / gridDim.x);
+    const int last = item_at_cost(L, L.total_cost * (int64_t)(blockIdx.x + 1) / gridDim.x);
+    APB_TS(0);
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (first >= last) return;
+
+    // ---- plane-load iterator: walks this warp's units across the item range.
+    // Items are contiguous and problems only advance, so everything is
+    // incremental (no search, no 64-bit multiply per unit).
+    int li_item = first, li_u = warp;
+    int li_pi = problem_of(L, first);
+    int li_pend = 0, li_units = 0;  // first item of the next problem; units per item
+    int64_t li_rows = 0, li_rb_bytes = 0, li_row0 = 0, li_pstride = 0;
+    const uint8_t* li_b0 = nullptr;
+    auto li_problem = [&]() {  // cache the fields of problem li_pi at item li_item
+        const GemvProblem& P = L.prob[li_pi];
+        li_pend = li_pi + 1 < L.n_prob ? L.prob[li_pi + 1].item_begin : L.n_items;
+        li_units = P.n_tiles * UPT;
+        li_rows = P.rows;
+        li_rb_bytes = P.row_bytes;
+        li_pstride = P.plane_stride;
+        li_row0 = (int64_t)(li_item - P.item_begin) * kRowsPerCta + g;
+        li_b0 = P.planes + li_row0 * P.row_bytes + q * UB;
+    };
+    auto li_skip_empty = [&]() {  // skip problems whose items have no unit for this warp
+        while (li_item < last && li_u >= li_units) {
+            li_item = li_pend;
+            if (li_item >= last) break;
+            ++li_pi;
+            li_problem();
+        }
+    };
+    auto li_load = [&](VT(&dst)[2][K]) {
+        if (li_item >= last) return;
+        const int tile = li_u / UPT, s = li_u - tile * UPT;
+        const uint8_t* p0 = li_b0 + (int64_t)tile * kTileBytes + s * 4 * UB;
+        const uint8_t* p1 = p0 + 8 * li_rb_bytes;
+        const bool ok0 = li_row0 < li_rows, ok1 = li_row0 + 8 < li_rows;
 #pragma unroll
         for (int p = 0; p < K; ++p) {
-            dst[0][K - 1 - p] = ok0 ? V::load(b0 + p * plane_stride) : V::zero();
-            dst[1][K - 1 - p] = ok1 ? V::load(b1 + p * plane_stride) : V::zero();
+            dst[0][K - 1 - p] = ok0 ? V::load(p0 + p * li_pstride) : V::zero();
+            dst[1][K - 1 - p] = ok1 ? V::load(p1 + p * li_pstride) : V::zero();
+        }
+        li_u += kWarps;
+        if (li_u >= li_units) {  // next item
+            li_u = warp;
+            ++li_item;
+            if (li_item < last) {
+                if (li_item >= li_pend) {
+                    ++li_pi;
+                    li_problem();
+                    li_skip_empty();
+                } else {
+                    li_row0 += kRowsPerCta;
+                    li_b0 += kRowsPerCta * li_rb_bytes;
+                }
+            }
         }
     };
 
+    // centroid rows of an item -> stage (cp.async, zero-filled past the last row)
+    auto stage_lut = [&](int item, int pi) {
+        const GemvProblem& P = L.prob[pi];
+        const int64_t rb = item - P.item_begin;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.lut) + rb * TG::kStageBytes;
+        const int64_t valid = (P.rows - rb * kRowsPerCta) * (int64_t)(2 << K);  // bytes
+        for (int c = tid; c < TG::kStageBytes / 16; c += nthreads) {
+            const int64_t o = (int64_t)c * 16;
+            const int64_t nb = valid - o;
+            cp_async16(stage + o, nb > 0 ? (const void*)(src + o) : (const void*)src,
+                       nb >= 16 ? 16 : (nb > 0 ? (int)nb : 0));
+        }
+    };
+    // replicated lookup tables from the staged centroid rows
+    auto build_table = [&]() {
+        const uint16_t* st = reinterpret_cast<const uint16_t*>(stage);
+        if constexpr (TG::kPair) {
+            // item (rl, ce): the 2^K entries (L[ce], L[co]) for every co
+            for (int it = tid; it < (kRowsPerCta << K); it += nthreads) {
+                const int rl = it & 15, ce = it >> 4;
+                const uint16_t* lr = st + (rl << K);
+                const uint32_t lce = lr[ce];
+                uint32_t sce = 0;  // code bit i -> pair-index bit 2i
+#pragma unroll
+                for (int i = 0; i < K; ++i) sce |= (((uint32_t)ce >> i) & 1u) << (2 * i);
+                uint8_t* dst = table + rl * 16 + sce * 256;
+#pragma unroll
+                for (int co = 0; co < (1 << K); ++co) {
+                    uint32_t sco = 0;
+#pragma unroll
+                    for (int i = 0; i < K; ++i) sco |= ((uint32_t)(co >> i) & 1u) << (2 * i + 1);
+                    const uint32_t v = lce | ((uint32_t)lr[co] << 16);
+                    *reinterpret_cast<uint4*>(dst + sco * 256) = make_uint4(v, v, v, v);
+                }
+            }
+        } else {
+            // item (rl, 8 consecutive entries)
+            for (int it = tid; it < kRowsPerCta * (1 << K) / 8; it += nthreads) {
+                const int rl = it & 15, e8 = it >> 4;
+                const uint4 h = lds128(stage + (rl << K) * 2 + e8 * 16);
+                uint8_t* dst = table + rl * 16 + e8 * 8 * 256;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t w = u4_word(h, j >> 1);
+                    const uint32_t v = (j & 1) ? (w >> 16) : (w & 0xFFFFu);
+                    *reinterpret_cast<uint4*>(dst + j * 256) = make_uint4(v, v, v, v);
+                }
+            }
+        }
+    };
+    // activations of a problem -> xs ([m_x][padded] fp16, zero beyond cols)
+    auto stage_x = [&](int pi) {
+        const GemvProblem& P = L.prob[pi];
+        const int64_t padded = (int64_t)P.n_tiles * kTileWeights;
+        const int chunks = (int)(padded / 8);
+        for (int m = 0; m < L.m_x; ++m) {
+            const uint16_t* srow = P.x + (int64_t)m * P.ldx;
+            uint8_t* drow = xs + (int64_t)m * padded * 2;
+            for (int c = tid; c < chunks; c += nthreads) {
+                const int64_t col = (int64_t)c * 8;
+                const int64_t nb = (P.cols - col) * 2;
+                cp_async16(drow + col * 2, nb > 0 ? (const void*)(srow + col) : (const void*)srow,
+                           nb >= 16 ? 16 : (nb > 0 ? (int)nb : 0));
+            }
+        }
+    };
+
+    // ---- prologue --------------------------------------------------------------
+    int cur_pi = li_pi;
+    stage_lut(first, cur_pi);
+    cp_async_commit();
     VT bufA[2][K], bufB[2][K];
-    int u = warp;
-    if (u < n_units) load_unit(u, bufA);
-
-    // ---- centroid tables -> replicated shared-memory lookup tables ----------
-    {
-        uint16_t* lut_s = reinterpret_cast<uint16_t*>(scratch);
-        constexpr int NL = kRowsPerCta << K;
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(lut + rb * kRowsPerCta * (1 << K));
-        const int64_t valid = (rows - rb * kRowsPerCta) << K;  // halves available
-        for (int i = tid; i < NL / 2; i += blockDim.x)
-            reinterpret_cast<uint32_t*>(lut_s)[i] = (2 * i < valid) ? __ldg(src + i) : 0u;
-        __syncthreads();
-        constexpr int NE = TableGeom<K>::kEntries;
-        for (int i = tid; i < NE * kRowsPerCta; i += blockDim.x) {
-            const int idx = i >> 4, rl = i & 15;
-            const uint16_t* lr = lut_s + (rl << K);
-            uint32_t v;
-            if constexpr (TableGeom<K>::kPair) {
-                uint32_t ce, co;
-                pair_codes<K>((uint32_t)idx, ce, co);
-                v = (uint32_t)lr[ce] | ((uint32_t)lr[co] << 16);
-            } else {
-                v = lr[idx];
-            }
-            *reinterpret_cast<uint4*>(table + idx * 256 + rl * 16) = make_uint4(v, v, v, v);
-        }
-        __syncthreads();
-    }
-
-    const uint32_t off0 = (uint32_t)lane * 4u, off1 = 128u + (uint32_t)lane * 4u;
-    const uint16_t* xrow[NG];
-#pragma unroll
-    for (int ng = 0; ng < NG; ++ng) {
-        const int m = min(g + 8 * ng, L.m_x - 1);
-        xrow[ng] = xg + (int64_t)m * ldx;
-    }
-    float acc[NG][4];
-#pragma unroll
-    for (int ng = 0; ng < NG; ++ng) acc[ng][0] = acc[ng][1] = acc[ng][2] = acc[ng][3] = 0.f;
-
-    auto compute_unit = [&](int uu, const VT (&buf)[2][K]) {
-        const int tile = uu / UPT, s = uu - tile * UPT;
-        const bool full_tile = (int64_t)(tile + 1) * kTileWeights <= cols;
-#pragma unroll
-        for (int w = 0; w < WPU; ++w) {
-            const int t = s * UB + q * WPU + w;  // lane word within the tile
-            const int64_t colbase = (int64_t)tile * kTileWeights + 8 * t;
-            uint4 xv[NG][4];
-            if (full_tile) {
-#pragma unroll
-                for (int ng = 0; ng < NG; ++ng)
-#pragma unroll
-                    for (int p = 0; p < 4; ++p)
-                        xv[ng][p] = __ldg(reinterpret_cast<const uint4*>(xrow[ng] + colbase + 256 * p));
-            } else {
-#pragma unroll
-                for (int ng = 0; ng < NG; ++ng)
-#pragma unroll
-                    for (int p = 0; p < 4; ++p)
-                        xv[ng][p] = load_x8_tail(xrow[ng], colbase + 256 * p, cols);
-            }
-            uint32_t Q0[K], Q1[K];
-#pragma unroll
-            for (int i = 0; i < K; ++i) {
-                Q0[i] = V::word(buf[0][i], w);
-                Q1[i] = V::word(buf[1][i], w);
-            }
-            uint32_t a0[16], a1[16];
-            decode_word<K>(Q0, table, off0, a0);
-            decode_word<K>(Q1, table, off1, a1);
-#pragma unroll
-            for (int p = 0; p < 4; ++p)
-#pragma unroll
-                for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-                    for (int ng = 0; ng < NG; ++ng)
-                        mma16816(acc[ng], a0[p * 4 + 2 * jj], a1[p * 4 + 2 * jj],
-                                 a0[p * 4 + 2 * jj + 1], a1[p * 4 + 2 * jj + 1],
-                                 u4_word(xv[ng][p], 2 * jj), u4_word(xv[ng][p], 2 * jj + 1));
-        }
-    };
-
-    // ---- main loop: double-buffered unit stream ------------------------------
-#pragma unroll 1
-    while (u < n_units) {
-        int un = u + nwarps;
-        if (un < n_units) load_unit(un, bufB);
-        compute_unit(u, bufA);
-        u = un;
-        if (u >= n_units) break;
-        un = u + nwarps;
-        if (un < n_units) load_unit(un, bufA);
-        compute_unit(u, bufB);
-        u = un;
-    }
-
-    // ---- fixed-order CTA reduction + store ---------------------------------
-    float* red = reinterpret_cast<float*>(scratch);  // [warp][16 rows][8*NG cols]
-    constexpr int RC = 8 * NG;
-#pragma unroll
-    for (int ng = 0; ng < NG; ++ng) {
-        float* r0p = red + (warp * kRowsPerCta + g) * RC + ng * 8 + 2 * q;
-        float* r1p = red + (warp * kRowsPerCta + g + 8) * RC + ng * 8 + 2 * q;
-        r0p[0] = acc[ng][0];
-        r0p[1] = acc[ng][1];
-        r1p[0] = acc[ng][2];
-        r1p[1] = acc[ng][3];
+    li_problem();
+    li_skip_empty();
+    li_load(bufA);
+    li_load(bufB);
+    APB_TS(1);
+    cp_async_wait_all();
+    __syncthreads();
+    build_table();
+    APB_TS(2);
+    // Programmatic dependent launch: everything above touches only weights
+    // (planes, tables); activations may come from the previous kernel in the
+    // stream, so wait for it here (no-op without PDL).
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (XS) {
+        stage_x(cur_pi);
+        cp_async_commit();
+        cp_async_wait_all();
     }
     __syncthreads();
+    APB_TS(3);
+
+    const uint32_t off0 = (uint32_t)lane * 4u, off1 = 128u + (uint32_t)lane * 4u;
     const int m_out = L.x_split ? (L.m_x >> 1) : L.m_x;
-    for (int i = tid; i < kRowsPerCta * m_out; i += blockDim.x) {
-        const int rl = i & 15, m = i >> 4;
-        const int64_t row = rb * kRowsPerCta + rl;
-        if (row >= rows) continue;
-        float s;
-        if (L.x_split) {
-            float hi = 0.f, lo = 0.f;
-            for (int w = 0; w < nwarps; ++w) hi += red[(w * kRowsPerCta + rl) * RC + 2 * m];
-            for (int w = 0; w < nwarps; ++w) lo += red[(w * kRowsPerCta + rl) * RC + 2 * m + 1];
-            s = hi + lo;
-        } else {
-            s = 0.f;
-            for (int w = 0; w < nwarps; ++w) s += red[(w * kRowsPerCta + rl) * RC + m];
+    int j = 0;  // ring position (A/B)
+
+#pragma unroll 1
+    for (int item = first; item < last; ++item) {
+        const GemvProblem& P = L.prob[cur_pi];
+        const int64_t rb = item - P.item_begin;
+        const int n_units = P.n_tiles * UPT;
+        const int64_t cols = P.cols;
+        const int64_t padded = (int64_t)P.n_tiles * kTileWeights;
+        const int nxt = item + 1;
+        const int cur_pend = cur_pi + 1 < L.n_prob ? L.prob[cur_pi + 1].item_begin : L.n_items;
+        const int nxt_pi = (nxt < last && nxt >= cur_pend) ? cur_pi + 1 : cur_pi;
+        // next block's centroid rows land in `stage` while this block computes
+        if (nxt < last) stage_lut(nxt, nxt_pi);
+        cp_async_commit();
+
+        int xm[NG];
+#pragma unroll
+        for (int ng = 0; ng < NG; ++ng) xm[ng] = min(g + 8 * ng, L.m_x - 1);
+        // two independent accumulator chains (even / odd 256-column run)
+        float acc[NG][2][4];
+#pragma unroll
+        for (int ng = 0; ng < NG; ++ng)
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2) acc[ng][c2][0] = acc[ng][c2][1] = acc[ng][c2][2] = acc[ng][c2][3] = 0.f;
+
+        auto compute_unit = [&](int uu, const VT(&buf)[2][K]) {
+            const int tile = uu / UPT, s = uu - tile * UPT;
+            const bool full_tile = XS || (int64_t)(tile + 1) * kTileWeights <= cols;
+#pragma unroll
+            for (int w = 0; w < WPU; ++w) {
+                const int t = s * UB + q * WPU + w;  // lane word within the tile
+                const int64_t colbase = (int64_t)tile * kTileWeights + 8 * t;
+                uint4 xv[NG][4];
+#pragma unroll
+                for (int ng = 0; ng < NG; ++ng)
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                        if constexpr (XS) {
+                            // only lanes holding a real batch column load x (the
+                            // B columns n >= m_x are never read back): with
+                            // m_x <= 2 that is one shared-memory wavefront, not 4
+                            xv[ng][p] = (g + 8 * ng < L.m_x)
+                                            ? lds128(xs + (xm[ng] * padded + colbase + 256 * p) * 2)
+                                            : make_uint4(0, 0, 0, 0);
+                        } else {
+                            const uint16_t* xr = P.x + (int64_t)xm[ng] * P.ldx;
+                            xv[ng][p] = full_tile ? __ldg(reinterpret_cast<const uint4*>(xr + colbase + 256 * p))
+                                                  : load_x8_tail(xr, colbase + 256 * p, cols);
+                        }
+                    }
+                uint32_t Q0[K], Q1[K];
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                    Q0[i] = V::word(buf[0][i], w);
+                    Q1[i] = V::word(buf[1][i], w);
+                }
+                uint32_t a0[16], a1[16];
+                decode_word<K>(Q0, off0, a0);
+                decode_word<K>(Q1, off1, a1);
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+                        for (int ng = 0; ng < NG; ++ng)
+                            mma16816(acc[ng][p & 1], a0[p * 4 + 2 * jj], a1[p * 4 + 2 * jj],
+                                     a0[p * 4 + 2 * jj + 1], a1[p * 4 + 2 * jj + 1],
+                                     u4_word(xv[ng][p], 2 * jj), u4_word(xv[ng][p], 2 * jj + 1));
+            }
+        };
+
+        // ---- this warp's units; the buffer just consumed is refilled with the
+        //      unit two steps ahead (possibly of the next item)
+#pragma unroll 1
+        for (int u = warp; u < n_units; u += kWarps) {
+            if (j & 1) {
+                compute_unit(u, bufB);
+                li_load(bufB);
+            } else {
+                compute_unit(u, bufA);
+                li_load(bufA);
+            }
+            ++j;
         }
-        if (L.y_f16)
-            reinterpret_cast<__half*>(yg)[(int64_t)m * ldy + row] = __float2half_rn(s);
-        else
-            reinterpret_cast<float*>(yg)[(int64_t)m * ldy + row] = s;
-    }
-}
 
-template <int K, int NG, int UB>
-static size_t smem_bytes(int nwarps) {
-    const size_t lut_stage = (size_t)kRowsPerCta * (1u << K) * 2;
-    const size_t red = (size_t)nwarps * kRowsPerCta * 8 * NG * 4;
-    return TableGeom<K>::kBytes + (lut_stage > red ? lut_stage : red);
-}
-
-template <int K, int NG, int UB>
-static int launch_variant(const GemvLaunch& L, int n_blocks, int nwarps, cudaStream_t s) {
-    static std::atomic<int> configured{0};
-    const size_t smem = smem_bytes<K, NG, UB>(GemvBounds<NG>::kThreads / 32);
-    if (!configured.load(std::memory_order_acquire)) {
-        if (cudaFuncSetAttribute(gemv_kernel<K, NG, UB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
-            return APB_ERR_CUDA;
-        configured.store(1, std::memory_order_release);
+        // ---- item boundary: fixed-order reduction + next table ---------------
+#pragma unroll
+        for (int ng = 0; ng < NG; ++ng) {
+            float* r0p = red + (warp * kRowsPerCta + g) * RC + ng * 8 + 2 * q;
+            float* r1p = red + (warp * kRowsPerCta + g + 8) * RC + ng * 8 + 2 * q;
+            r0p[0] = acc[ng][0][0] + acc[ng][1][0];
+            r0p[1] = acc[ng][0][1] + acc[ng][1][1];
+            r1p[0] = acc[ng][0][2] + acc[ng][1][2];
+            r1p[1] = acc[ng][0][3] + acc[ng][1][3];
+        }
+        cp_async_wait_all();  // next block's centroid rows
+        __syncthreads();      // S1: table / xs / red free or complete
+        APB_TS(4);
+        for (int i = tid; i < kRowsPerCta * m_out; i += nthreads) {
+            const int rl = i & 15, m = i >> 4;
+            const int64_t row = rb * kRowsPerCta + rl;
+            if (row >= P.rows) continue;
+            float sum;
+            if (L.x_split) {
+                float hi = 0.f, lo = 0.f;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) hi += red[(w * kRowsPerCta + rl) * RC + 2 * m];
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) lo += red[(w * kRowsPerCta + rl) * RC + 2 * m + 1];
+                sum = hi + lo;
+            } else {
+                sum = 0.f;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) sum += red[(w * kRowsPerCta + rl) * RC + m];
+            }
+            if (L.y_f16)
+                reinterpret_cast<__half*>(P.y)[(int64_t)m * P.ldy + row] = __float2half_rn(sum);
+            else
+                reinterpret_cast<float*>(P.y)[(int64_t)m * P.ldy + row] = sum;
+        }
+        if (nxt < last) {
+            build_table();
+            if constexpr (XS) {
+                if (nxt_pi != cur_pi) {  // new layer: restage its activations
+                    stage_x(nxt_pi);
+                    cp_async_commit();
+                    cp_async_wait_all();
+                }
+            }
+        }
+        cur_pi = nxt_pi;
+        __syncthreads();  // S2
     }
-    gemv_kernel<K, NG, UB><<<n_blocks, nwarps * 32, smem_bytes<K, NG, UB>(nwarps), s>>>(L);
-    return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
+    APB_TS(5);
 }
 
 template <int K, int NG>
-static int dispatch_ub(const GemvLaunch& L, int n_blocks, int nwarps, cudaStream_t s) {
-    if constexpr (K <= 5) return launch_variant<K, NG, 16>(L, n_blocks, nwarps, s);
-    else return launch_variant<K, NG, 8>(L, n_blocks, nwarps, s);
+static size_t smem_bytes(int64_t xs_bytes) {
+    return (size_t)TableGeom<K>::kBytes + TableGeom<K>::kStageBytes +
+           (size_t)kWarps * kRowsPerCta * 8 * NG * 4 + (size_t)xs_bytes;
+}
+
+constexpr int64_t kMaxXsBytes = 48 * 1024;
+
+static int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (cached[dev] == 0) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+        cached[dev] = n;
+    }
+    return cached[dev];
+}
+
+template <int K, int NG, int UB, bool XS>
+static int launch_variant(const GemvLaunch& L, cudaStream_t s) {
+    auto kern = gemv_kernel<K, NG, UB, XS>;
+    static std::atomic<int> configured{0};
+    if (!configured.load(std::memory_order_acquire)) {
+        const size_t max_smem = smem_bytes<K, NG>(XS ? kMaxXsBytes : 0);
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem) != cudaSuccess)
+            return APB_ERR_CUDA;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+            return APB_ERR_CUDA;
+        configured.store(1, std::memory_order_release);
+    }
+    const size_t smem = smem_bytes<K, NG>(XS ? L.xs_bytes : 0);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GemvBounds<NG>::kThreads, smem) !=
+            cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    int grid = per_sm * sm_count();
+    if (grid > L.n_items) grid = L.n_items;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)GemvBounds<NG>::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (L.flags & APB_FLAG_PDL) ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, kern, L) != cudaSuccess) return APB_ERR_CUDA;
+    return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
 }
 
 template <int K>
-static int dispatch_ng(int ng, const GemvLaunch& L, int n_blocks, int nwarps, cudaStream_t s) {
-    switch (ng) {
-        case 1: return dispatch_ub<K, 1>(L, n_blocks, nwarps, s);
-        case 2: return dispatch_ub<K, 2>(L, n_blocks, nwarps, s);
-        default: return dispatch_ub<K, 4>(L, n_blocks, nwarps, s);
-    }
+constexpr int unit_bytes() {
+    return K <= 3 ? 16 : 8;
 }
 
-static int units_per_tile(int k) { return k <= 5 ? 2 : 4; }
+template <int K, int NG>
+static int dispatch_xs(const GemvLaunch& L, cudaStream_t s) {
+    if constexpr (NG == 1) {
+        if (L.xs_bytes > 0) return launch_variant<K, NG, unit_bytes<K>(), true>(L, s);
+    }
+    return launch_variant<K, NG, unit_bytes<K>(), false>(L, s);
+}
 
-// Warps per CTA: a divisor of the unit count in [4, 12] when one exists
-// (balanced K split), otherwise 8.
-static int pick_warps(int n_units, int max_warps) {
-    for (int w = 8; w >= 4; --w)
-        if (n_units % w == 0) return w;
-    for (int w = 9; w <= max_warps; ++w)
-        if (n_units % w == 0) return w;
-    return n_units < 8 ? (n_units < 1 ? 1 : n_units) : 8;
+template <int K>
+static int dispatch_ng(int ng, const GemvLaunch& L, cudaStream_t s) {
+    switch (ng) {
+        case 1: return dispatch_xs<K, 1>(L, s);
+        case 2: return dispatch_xs<K, 2>(L, s);
+        default: return dispatch_xs<K, 4>(L, s);
+    }
 }
 
 }  // namespace apb
 
 using namespace apb;
 
-static int gemv_launch_chunk(int n, const uint8_t* const* planes, const int* n_max,
-                             const int64_t* rows, const int64_t* cols, const int64_t* padded, int k,
+static int gemv_launch_chunk(int n, const uint8_t* const* planes, const int64_t* rows,
+                             const int64_t* cols, const int64_t* padded, int k,
                              const uint16_t* const* lut, const uint16_t* const* x, int m_x,
                              const int64_t* ldx, int64_t x_off, int x_split, void* const* y,
-                             int y_dtype, const int64_t* ldy, int64_t y_off, cudaStream_t s) {
+                             int y_dtype, const int64_t* ldy, int64_t y_off, int flags,
+                             cudaStream_t s) {
     GemvLaunch L;
+    L.flags = flags;
     L.n_prob = n;
     L.m_x = m_x;
     L.x_split = x_split;
     L.y_f16 = y_dtype == APB_DTYPE_F16;
-    int blocks = 0, max_units = 0;
+    int items = 0;
+    int64_t cost = 0, max_padded = 0;
     const int esz = y_dtype == APB_DTYPE_F16 ? 2 : 4;
     for (int i = 0; i < n; ++i) {
         GemvProblem& P = L.prob[i];
@@ -401,21 +642,26 @@ static int gemv_launch_chunk(int n, const uint8_t* const* planes, const int* n_m
         P.ldx = ldx[i];
         P.ldy = ldy[i];
         P.n_tiles = (int)(padded[i] / kTileWeights);
-        P.block_begin = blocks;
-        blocks += (int)((rows[i] + kRowsPerCta - 1) / kRowsPerCta);
-        const int nu = P.n_tiles * units_per_tile(k);
-        if (nu > max_units) max_units = nu;
+        P.item_begin = items;
+        P.cost_begin = cost;
+        const int n_items = (int)((rows[i] + kRowsPerCta - 1) / kRowsPerCta);
+        items += n_items;
+        cost += (int64_t)n_items * P.n_tiles;
+        if (padded[i] > max_padded) max_padded = padded[i];
     }
+    L.n_items = items;
+    L.total_cost = cost;
     const int ng = m_x <= 8 ? 1 : (m_x <= 16 ? 2 : 4);
-    const int nwarps = pick_warps(max_units, ng == 1 ? 12 : 8);
+    const int64_t xs = (int64_t)m_x * max_padded * 2;
+    L.xs_bytes = (ng == 1 && xs <= kMaxXsBytes) ? xs : 0;
     switch (k) {
-        case 2: return dispatch_ng<2>(ng, L, blocks, nwarps, s);
-        case 3: return dispatch_ng<3>(ng, L, blocks, nwarps, s);
-        case 4: return dispatch_ng<4>(ng, L, blocks, nwarps, s);
-        case 5: return dispatch_ng<5>(ng, L, blocks, nwarps, s);
-        case 6: return dispatch_ng<6>(ng, L, blocks, nwarps, s);
-        case 7: return dispatch_ng<7>(ng, L, blocks, nwarps, s);
-        case 8: return dispatch_ng<8>(ng, L, blocks, nwarps, s);
+        case 2: return dispatch_ng<2>(ng, L, s);
+        case 3: return dispatch_ng<3>(ng, L, s);
+        case 4: return dispatch_ng<4>(ng, L, s);
+        case 5: return dispatch_ng<5>(ng, L, s);
+        case 6: return dispatch_ng<6>(ng, L, s);
+        case 7: return dispatch_ng<7>(ng, L, s);
+        case 8: return dispatch_ng<8>(ng, L, s);
     }
     return APB_ERR_PARAM;
 }
@@ -424,21 +670,21 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
                                 const int64_t* rows, const int64_t* cols,
                                 const int64_t* padded_cols, int k, const uint16_t* const* lut,
                                 const uint16_t* const* x, int m_x, const int64_t* ldx, int x_split,
-                                void* const* y, int y_dtype, const int64_t* ldy, void* stream) {
+                                void* const* y, int y_dtype, const int64_t* ldy, int flags,
+                                void* stream) {
     if (n_problems < 1) return APB_ERR_SHAPE;
     if (k < 2 || k > 8) return APB_ERR_PARAM;
     if (y_dtype != APB_DTYPE_F32 && y_dtype != APB_DTYPE_F16) return APB_ERR_PARAM;
     if (m_x < 1 || (x_split && (m_x & 1))) return APB_ERR_SHAPE;
-    const int m_out = x_split ? m_x / 2 : m_x;
     for (int i = 0; i < n_problems; ++i) {
         if (rows[i] <= 0 || cols[i] <= 0) return APB_ERR_SHAPE;
         if (padded_cols[i] != apb_pad_columns(cols[i])) return APB_ERR_SHAPE;
         if (k > n_max[i] || n_max[i] > 8) return APB_ERR_PARAM;
         if (ldx[i] < cols[i] || (ldx[i] % 8) != 0) return APB_ERR_PARAM;
-        if (((uintptr_t)x[i] & 15) != 0 || ((uintptr_t)planes[i] & 15) != 0) return APB_ERR_PARAM;
-        if (((uintptr_t)lut[i] & 3) != 0) return APB_ERR_PARAM;
-        if (ldy[i] < rows[i]) return APB_ERR_SHAPE;
         if (!planes[i] || !lut[i] || !x[i] || !y[i]) return APB_ERR_PARAM;
+        if (((uintptr_t)x[i] & 15) != 0 || ((uintptr_t)planes[i] & 15) != 0) return APB_ERR_PARAM;
+        if (((uintptr_t)lut[i] & 15) != 0) return APB_ERR_PARAM;
+        if (ldy[i] < rows[i]) return APB_ERR_SHAPE;
     }
     cudaStream_t s = (cudaStream_t)stream;
     // batch columns per launch: 32 fp16 activation rows (4 mma column groups)
@@ -447,20 +693,25 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
         const int n = n_problems - p0 < kMaxGroup ? n_problems - p0 : kMaxGroup;
         for (int m0 = 0; m0 < m_x; m0 += chunk) {
             const int mc = m_x - m0 < chunk ? m_x - m0 : chunk;
-            const int rc = gemv_launch_chunk(n, planes + p0, n_max + p0, rows + p0, cols + p0,
-                                             padded_cols + p0, k, lut + p0, x + p0, mc, ldx + p0,
-                                             m0, x_split, y + p0, y_dtype, ldy + p0,
-                                             x_split ? m0 / 2 : m0, s);
+            const int rc = gemv_launch_chunk(n, planes + p0, rows + p0, cols + p0, padded_cols + p0, k,
+                                             lut + p0, x + p0, mc, ldx + p0, m0, x_split, y + p0,
+                                             y_dtype, ldy + p0, x_split ? m0 / 2 : m0, flags, s);
             if (rc != APB_OK) return rc;
         }
     }
-    (void)m_out;
     return APB_OK;
 }
 
+#ifdef APB_TIMELINE
+extern "C" int apb_debug_set_timeline(unsigned long long* p) {
+    return cudaMemcpyToSymbol(g_timeline, &p, sizeof(p)) == cudaSuccess ? APB_OK : APB_ERR_CUDA;
+}
+#endif
+
 extern "C" int apb_gemv(const uint8_t* planes, int n_max, int64_t rows, int64_t cols,
                         int64_t padded_cols, int k, const uint16_t* lut, const uint16_t* x, int m_x,
-                        int64_t ldx, int x_split, void* y, int y_dtype, int64_t ldy, void* stream) {
+                        int64_t ldx, int x_split, void* y, int y_dtype, int64_t ldy, int flags,
+                        void* stream) {
     return apb_gemv_grouped(1, &planes, &n_max, &rows, &cols, &padded_cols, k, &lut, &x, m_x, &ldx,
-                            x_split, &y, y_dtype, &ldy, stream);
+                            x_split, &y, y_dtype, &ldy, flags, stream);
 }

@@ -253,7 +253,7 @@ def _quantized(prep: PreparedLayer, x2, k: int, fp16: bool):
     check(
         load().apb_gemv(dev.ptr(t.planes), t.n_max, t.rows, t.cols, t.padded_cols, k,
                         dev.ptr(prep.tables16[k]), dev.ptr(xdev), m_x, ldx, split, dev.ptr(y),
-                        APB_DTYPE_F32, t.rows, dev.stream_ptr()),
+                        APB_DTYPE_F32, t.rows, 0, dev.stream_ptr()),
         "apb_gemv",
     )
     if kind == "numpy":

@@ -13,7 +13,16 @@ from __future__ import annotations
 import ctypes
 
 from . import _device as dev
-from ._lib import APB_DTYPE_F16, APB_DTYPE_F32, check, int64_array, int_array, load, ptr_array
+from ._lib import (
+    APB_DTYPE_F16,
+    APB_DTYPE_F32,
+    APB_FLAG_PDL,
+    check,
+    int64_array,
+    int_array,
+    load,
+    ptr_array,
+)
 from .errors import ParameterError
 
 
@@ -23,7 +32,7 @@ def _ldx(cols: int) -> int:
 
 class GemvPlan:
     def __init__(self, preps, k: int, m: int = 1, grouped: bool = True, x_split: bool = False,
-                 y_fp16: bool = False):
+                 y_fp16: bool = False, pdl: bool = False):
         torch = dev.require_cuda()
         for p in preps:
             if k not in p.tables16:
@@ -35,6 +44,9 @@ class GemvPlan:
         self.x_split = 1 if x_split else 0
         self.m_x = 2 * m if x_split else m
         self.y_dtype = APB_DTYPE_F16 if y_fp16 else APB_DTYPE_F32
+        # programmatic dependent launch: safe here because the plan's weights
+        # are never written by the kernels that precede it in a decode loop
+        self.flags = APB_FLAG_PDL if pdl else 0
         ydt = torch.float16 if y_fp16 else torch.float32
         self.x = [torch.zeros((self.m_x, _ldx(p.tensor.cols)), dtype=torch.float16, device="cuda")
                   for p in self.preps]
@@ -75,7 +87,7 @@ class GemvPlan:
                                    ctypes.cast(self._xp, ctypes.POINTER(ctypes.c_void_p)),
                                    self.m_x, self._ldx, self.x_split,
                                    ctypes.cast(self._yp, ctypes.POINTER(ctypes.c_void_p)),
-                                   self.y_dtype, self._ldy, s),
+                                   self.y_dtype, self._ldy, self.flags, s),
                 "apb_gemv_grouped",
             )
             return
@@ -83,7 +95,8 @@ class GemvPlan:
             check(
                 L.apb_gemv(self._planes[i], self._nmax[i], self._rows[i], self._cols[i],
                            self._padded[i], self.k, self._lut[i], self._xp[i], self.m_x,
-                           self._ldx[i], self.x_split, self._yp[i], self.y_dtype, self._ldy[i], s),
+                           self._ldx[i], self.x_split, self._yp[i], self.y_dtype, self._ldy[i],
+                           self.flags, s),
                 "apb_gemv",
             )
 

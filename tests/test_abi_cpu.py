@@ -59,15 +59,15 @@ def test_host_validation_before_launch(lib):
     nul = ctypes.c_void_p(0)
     fake = ctypes.c_void_p(0x1000)
     # k outside [2, 8]
-    assert lib.apb_gemv(fake, 8, 16, 1024, 1024, 9, fake, fake, 1, 1024, 0, fake, 0, 16, nul) == 2
+    assert lib.apb_gemv(fake, 8, 16, 1024, 1024, 9, fake, fake, 1, 1024, 0, fake, 0, 16, 0, nul) == 2
     # padded columns inconsistent
-    assert lib.apb_gemv(fake, 8, 16, 1024, 2048, 4, fake, fake, 1, 1024, 0, fake, 0, 16, nul) == 1
+    assert lib.apb_gemv(fake, 8, 16, 1024, 2048, 4, fake, fake, 1, 1024, 0, fake, 0, 16, 0, nul) == 1
     # misaligned activations (ldx % 8)
-    assert lib.apb_gemv(fake, 8, 16, 1000, 1024, 4, fake, fake, 1, 1001, 0, fake, 0, 16, nul) == 2
+    assert lib.apb_gemv(fake, 8, 16, 1000, 1024, 4, fake, fake, 1, 1001, 0, fake, 0, 16, 0, nul) == 2
     # k > n_max
-    assert lib.apb_gemv(fake, 4, 16, 1024, 1024, 5, fake, fake, 1, 1024, 0, fake, 0, 16, nul) == 2
+    assert lib.apb_gemv(fake, 4, 16, 1024, 1024, 5, fake, fake, 1, 1024, 0, fake, 0, 16, 0, nul) == 2
     # odd hi/lo activation count
-    assert lib.apb_gemv(fake, 8, 16, 1024, 1024, 4, fake, fake, 3, 1024, 1, fake, 0, 16, nul) == 1
+    assert lib.apb_gemv(fake, 8, 16, 1024, 1024, 4, fake, fake, 3, 1024, 1, fake, 0, 16, 0, nul) == 1
     # pack: n_max out of range, empty matrix
     assert lib.apb_pack(fake, 4, 4, 4, 9, 1, fake, nul, nul) == 2
     assert lib.apb_pack(fake, 0, 4, 4, 3, 1, fake, nul, nul) == 1
