@@ -3,18 +3,25 @@
 Workload (BASELINE.json configs[1]): the Llama-2-7B decode layer set
 (q/k/v/o 4096x4096, gate/up 11008x4096, down 4096x11008), 8-bit parent
 bitplanes + per-row fp16 centroid tables, batch 1, every child bit-width
-k = 3..8.  One STEP = the 7 GEMVs at each of k = 3..8 (42 launches).
+k = 3..8.  One STEP = the 7 GEMVs at each of k = 3..8.  Within a k the GEMVs
+are launched the way a decode block issues them: one grouped launch for
+q/k/v (shared activation), o, one grouped launch for gate/up (shared
+activation), down -- 4 launches per k, 24 per step, chained with programmatic
+dependent launch and replayed from a CUDA graph.
 
-metric/value: whole-job algorithmic HBM GB/s = sum of SURVEY.md section 8(d)
-bytes (R*C*k/8 + R*2^k*2 + C*2 + R*2 per GEMV) / device time (CUDA events,
-max over ranks).  Inputs live in HBM; the weights are rotated over 4 copies
-(4 x 203 MB) so no GEMV finds its planes in the 126 MB L2.
+value: whole-job algorithmic HBM GB/s = sum of SURVEY.md section 8(d) bytes
+(R*C*k/8 + R*2^k*2 + C*2 + R*2 per GEMV) / device time (CUDA events on the
+launch stream, max over ranks).  Inputs are resident in HBM; the weights are
+rotated over 4 copies (4 x 203 MB) per launch, so no launch finds its planes in
+the 126 MB L2.  With N > 1 GPUs every layer is row-sharded (rank i holds rows
+[i*R/N, (i+1)*R/N)) and each GEMV is followed by an NCCL all-gather of the
+output slices (strong scaling: total work fixed).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 --impl reference times the CPU oracle (oracle/anyprec_oracle.c, a C port of
-the reference engine) on all host cores -- the reference package itself is
-numpy-only and publishes no numbers.
+the reference engine; the reference package itself is numpy-only and
+publishes no numbers) on all host cores.
 """
 
 from __future__ import annotations
@@ -35,6 +42,7 @@ sys.path.insert(0, ROOT)
 
 SHAPES = [("q", 4096, 4096), ("k", 4096, 4096), ("v", 4096, 4096), ("o", 4096, 4096),
           ("gate", 11008, 4096), ("up", 11008, 4096), ("down", 4096, 11008)]
+GROUPS = [[0, 1, 2], [3], [4, 5], [6]]  # decode-block launch groups (shared x within a group)
 BITS = [3, 4, 5, 6, 7, 8]
 N_MAX = 8
 N_COPIES = 4
@@ -46,7 +54,7 @@ def alg_bytes(rows: int, cols: int, k: int, m: int = 1) -> int:
     return rows * cols * k // 8 + rows * (1 << k) * 2 + m * cols * 2 + m * rows * 2
 
 
-def step_bytes(shapes, m: int = 1) -> int:
+def step_bytes(shapes=SHAPES, m: int = 1) -> int:
     return sum(alg_bytes(r, c, k, m) for k in BITS for _, r, c in shapes)
 
 
@@ -79,6 +87,7 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            time.sleep(0.15)
         except Exception:
             self.proc = None
         return self
@@ -119,18 +128,18 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # our arm
 
-def make_layer_set(torch, seed: int, rank: int, world: int):
-    """Random-init layer set on the device: codes U[0,256), sorted N(0,1)
-    fp16 tables per k (helpers.random_layer semantics).
-    With world > 1 each rank holds its contiguous row shard."""
+def make_layer_set(torch, seed: int, rank: int = 0, world: int = 1):
+    """Random-init layer set on the device: codes U[0,256), sorted N(0,1) fp16
+    tables per k (helpers.random_layer semantics).  With
+    world > 1 each rank builds only its contiguous row shard."""
     from paper_2402_10517_b200 import AnyPrecisionLayer, engine
+    from paper_2402_10517_b200.dist import shard_bounds
 
     g = torch.Generator(device="cuda").manual_seed(seed)
     preps = []
     for _, rows, cols in SHAPES:
-        r0, r1 = rows * rank // world, rows * (rank + 1) // world
-        codes = torch.randint(0, 256, (r1 - r0, cols), dtype=torch.uint8, device="cuda",
-                              generator=g)
+        r0, r1 = shard_bounds(rows, world, rank)
+        codes = torch.randint(0, 256, (r1 - r0, cols), dtype=torch.uint8, device="cuda", generator=g)
         tables = {k: torch.sort(torch.randn(r1 - r0, 1 << k, device="cuda", generator=g),
                                 dim=1).values.half() for k in range(3, 9)}
         layer = AnyPrecisionLayer(n_min=3, n_max=N_MAX, codes=codes, centroid_tables=tables,
@@ -140,11 +149,44 @@ def make_layer_set(torch, seed: int, rank: int, world: int):
     return preps
 
 
+def decode_plans(plan_mod, copies, pdl: bool):
+    """Per k: grouped q/k/v, o, grouped gate/up, down; weight copy rotated per launch."""
+    plans, i = [], 0
+    for k in BITS:
+        for grp in GROUPS:
+            c = copies[i % len(copies)]
+            p = plan_mod.GemvPlan([c[j] for j in grp], k, m=1, grouped=True, pdl=pdl,
+                                  shared_x=len(grp) > 1)
+            p.x[0].normal_()
+            plans.append((k, grp, p))
+            i += 1
+    return plans
+
+
+def time_graph(torch, fn, reps: int):
+    """Capture fn into a CUDA graph; return (graph, ms per replay)."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return g, a.elapsed_time(b) / reps
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2402_10517_b200 import plan
+    from paper_2402_10517_b200.dist import gather_rows
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -155,56 +197,30 @@ def run_ours(args):
     peak, peak_kind = peaks()
 
     copies = [make_layer_set(torch, 1234 + c, rank, world) for c in range(N_COPIES)]
-    # one plan per (k, layer, copy): per-GEMV launches, copy rotated per launch
-    plans = []
-    i = 0
-    for k in BITS:
-        for li in range(len(SHAPES)):
-            p = plan.GemvPlan([copies[i % N_COPIES][li]], k, m=1, grouped=False)
-            p.x[0][:, : SHAPES[li][2]].normal_()
-            plans.append((k, li, p))
-            i += 1
-    gathers = []
-    if world > 1:
-        for k, li, p in plans:
-            rows = SHAPES[li][1]
-            full = torch.empty((world, -(-rows // world)), dtype=torch.float32, device="cuda")
-            gathers.append(full)
+    plans = decode_plans(plan, copies, pdl=True)
 
     def step():
-        for j, (k, li, p) in enumerate(plans):
+        for k, grp, p in plans:
             p.run()
             if world > 1:
-                y = p.y[0][0]
-                pad = torch.nn.functional.pad(y, (0, gathers[j].shape[1] - y.shape[0]))
-                dist.all_gather_into_tensor(gathers[j], pad)
+                for j, li in enumerate(grp):
+                    gather_rows(p.y[j], SHAPES[li][1])
 
     # warm-up (also configures kernel attributes before capture)
-    for _ in range(max(1, args.warmup)):
+    for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     graph = None
-    if world == 1:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            step()
-        for _ in range(args.warmup):
-            graph.replay()
-        torch.cuda.synchronize()
+    try:
+        graph, _ = time_graph(torch, step, 1)
+    except Exception as e:  # NCCL capture not available: eager launches
+        print(f"[bench] CUDA graph capture failed ({e}); timing eager launches", file=sys.stderr)
+        graph = None
+    for _ in range(args.warmup):
+        graph.replay() if graph is not None else step()
+    torch.cuda.synchronize()
 
-    # per-launch durations (separate pass, events per launch) for the detail table
-    per = {}
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in plans]
-    for _ in range(3):
-        for (k, li, p), (a, b) in zip(plans, ev):
-            a.record()
-            p.run()
-            b.record()
-        torch.cuda.synchronize()
-        for (k, li, p), (a, b) in zip(plans, ev):
-            per.setdefault((k, li), []).append(a.elapsed_time(b) * 1e3)
-
-    # ---- timed region ------------------------------------------------------
+    # ---- timed region: K steps, barrier + synchronize on both sides --------
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -226,68 +242,80 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     clocks = clk.summary()
-
-    full_step_bytes = step_bytes([(n, r, c) for n, r, c in SHAPES])
     ms_per_step = ms / args.steps
-    value = full_step_bytes / (ms_per_step * 1e-3) / 1e9
+    value = step_bytes() / (ms_per_step * 1e-3) / 1e9
     launches = len(plans) * args.steps
-
-    # grouped launch (all 7 layers of one k in one kernel), for reference
-    gp = [plan.GemvPlan(copies[c], k, m=1, grouped=True) for c in range(N_COPIES) for k in BITS]
-    for p in gp:
-        p.run()
-    torch.cuda.synchronize()
-    gs, ge = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 20
-    gs.record()
-    for _ in range(reps):
-        for p in gp:
-            p.run()
-    ge.record()
-    torch.cuda.synchronize()
-    grouped_gbs = sum(p.algorithmic_bytes() for p in gp) * reps / (gs.elapsed_time(ge) * 1e-3) / 1e9
-
-    detail = {}
-    for k in BITS:
-        for li, (name, rows, cols) in enumerate(SHAPES):
-            us = statistics.median(per[(k, li)])
-            b = alg_bytes(rows, cols, k)
-            detail.setdefault(f"k{k}", {})[f"{name}_{rows}x{cols}"] = {
-                "us": round(us, 3), "GBps": round(b / (us * 1e-6) / 1e9, 1)}
 
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f16 x f16 -> f32 accumulate (u8 bitplanes)", "data": "synthetic random-init",
-        "config": {"workload": "llama2-7b decode layer set, 1 B200" if world == 1 else
-                   f"llama2-7b decode layer set, row-sharded over {world} B200 + NCCL all-gather",
+        "config": {"workload": "llama2-7b decode layer set (configs[1])" + (
+                       "" if world == 1 else f", rows sharded over {world} GPUs + NCCL all-gather"),
                    "shapes": [f"{n}:{r}x{c}" for n, r, c in SHAPES], "bits": BITS, "batch": 1,
-                   "n_max": N_MAX, "launches_per_step": len(plans), "cuda_graph": graph is not None,
-                   "l2": f"weights rotated over {N_COPIES} copies per launch (inputs > 2x L2)"},
+                   "n_max": N_MAX, "launch_groups": "qkv | o | gate+up | down per k (PDL chain)",
+                   "launches_per_step": len(plans), "cuda_graph": graph is not None,
+                   "l2": f"inputs > L2: weights rotated over {N_COPIES} copies (4 x 203 MB) per launch"},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": round(value, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(value / peak, 4), "peak_kind": peak_kind, "traffic": None},
+                     "frac": round(value / peak, 4), "peak_kind": peak_kind, "traffic": None,
+                     "note": "achieved = algorithmic bytes / CUDA-event time of the timed region "
+                             "(every launch in it is the GEMV kernel)"},
         "clocks": clocks,
-        "grouped_GBps": round(grouped_gbs, 1),
-        "per_gemv": detail,
     }
+    if world == 1:
+        result["per_gemv_us"] = per_gemv_detail(torch, plan, copies)
+        result["grouped_all7_GBps"] = grouped_all7(torch, plan, copies)
     if rank == 0:
-        result["e2e"] = run_e2e(torch, copies[0])
-        result["cpu_baseline"] = cpu_baseline(sample="one")
+        result["e2e"] = run_e2e(torch, copies[0], world)
+        if world == 1:
+            result["cpu_baseline"] = cpu_baseline()
         print(json.dumps(result))
     if world > 1:
         dist.destroy_process_group()
 
 
-def run_e2e(torch, preps, steps: int = 5):
+def per_gemv_detail(torch, plan, copies):
+    """Each GEMV alone: a PDL chain of 4 x 5 identical launches (rotating
+    copies) in a graph; µs per launch and GB/s."""
+    out = {}
+    for k in BITS:
+        for li, (n, r, c) in enumerate(SHAPES):
+            ps = [plan.GemvPlan([copies[j][li]], k, grouped=False, pdl=True) for j in range(N_COPIES)]
+
+            def chain():
+                for _ in range(5):
+                    for p in ps:
+                        p.run()
+
+            _, ms = time_graph(torch, chain, 10)
+            us = ms * 1e3 / (5 * len(ps))
+            out.setdefault(f"k{k}", {})[f"{n}_{r}x{c}"] = {
+                "us": round(us, 2), "GBps": round(alg_bytes(r, c, k) / (us * 1e-6) / 1e9, 1)}
+    return out
+
+
+def grouped_all7(torch, plan, copies):
+    ps = [plan.GemvPlan(copies[j % N_COPIES], k, grouped=True, pdl=True) for j, k in enumerate(BITS)]
+
+    def step():
+        for p in ps:
+            p.run()
+
+    _, ms = time_graph(torch, step, 20)
+    return round(step_bytes() / (ms * 1e-3) / 1e9, 1)
+
+
+def run_e2e(torch, preps, world, steps: int = 5):
     """Same metric through the public drop-in API with host buffers:
-    engine.gemv(prep, x_host_pinned_fp16) -> host y, per GEMV, k = 3..8."""
+    engine.gemv(prep, pinned host fp16 x) -> host y, one call per GEMV, k=3..8
+    (H2D of x and D2H of y inside the timed region)."""
     from paper_2402_10517_b200 import engine
 
     xs = [torch.randn(c, dtype=torch.float16).pin_memory() for _, _, c in SHAPES]
     h2d = sum(x.numel() * 2 for x in xs) * len(BITS)
-    d2h = sum(r * 4 for _, r, _ in SHAPES) * len(BITS)
+    d2h = sum(p.tensor.rows * 4 for p in preps) * len(BITS)
     for k in BITS:  # warm-up
         for p, x in zip(preps, xs):
             engine.gemv(p, x, engine.GemvConfig(bit_width=k, activations_fp16=True))
@@ -300,23 +328,23 @@ def run_e2e(torch, preps, steps: int = 5):
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
     assert not y.is_cuda
-    return {"value": round(step_bytes(SHAPES) / dt / 1e9, 2), "unit": "GB/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": round(dt * 1e3, 3), "api": "engine.gemv(host pinned fp16 x) -> host y"}
+    return {"value": round(step_bytes() / world / dt / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 3),
+            "api": "engine.gemv(prep, pinned host fp16 x) -> host y, 42 calls per step"
+                   + ("" if world == 1 else " (rank 0 shard only)")}
 
 
 # ---------------------------------------------------------------------------
 # CPU oracle (reference arm / cpu_baseline)
 
-def _oracle_layer_set(seed: int, shapes):
+def _oracle_layer_set(seed: int):
     from oracle import oracle as ora
 
     rng = np.random.default_rng(seed)
     out = []
-    for _, rows, cols in shapes:
+    for _, rows, cols in SHAPES:
         codes = rng.integers(0, 256, size=(rows, cols), dtype=np.uint8)
-        tables = {k: np.sort(rng.normal(size=(rows, 1 << k)), axis=1).astype(np.float16)
-                  for k in BITS}
+        tables = {k: np.sort(rng.normal(size=(rows, 1 << k)), axis=1).astype(np.float16) for k in BITS}
         planes = ora.permute(ora.pack_bitplanes(codes, N_MAX))
         x = rng.standard_normal(cols).astype(np.float16).astype(np.float32)
         out.append((planes, cols, tables, x))
@@ -331,16 +359,16 @@ def _oracle_step(ls, threads: int):
             ora.gemm(planes, cols, k, tables[k], x, nthreads=threads)
 
 
-def cpu_baseline(sample: str = "one"):
-    """The oracle C port timed on the host: 1 thread, one full step (the
-    7-layer set at k = 3..8) -- about 10-30 s of CPU work."""
-    ls = _oracle_layer_set(99, SHAPES)
+def cpu_baseline():
+    """The oracle C port on the host: 1 thread, one full step (7 layers x
+    k = 3..8) -- about 5-15 s of CPU work."""
+    ls = _oracle_layer_set(99)
     t0 = time.perf_counter()
     _oracle_step(ls, 1)
     dt = time.perf_counter() - t0
-    return {"value": round(step_bytes(SHAPES) / dt / 1e9, 4), "unit": "GB/s", "cores": 1,
-            "kind": "port", "sample": "one full step (7 layers x k=3..8), 1 thread, "
-            "oracle/anyprec_oracle.c", "seconds": round(dt, 2)}
+    return {"value": round(step_bytes() / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": "one full step (7 layers x k=3..8), 1 thread, oracle/anyprec_oracle.c "
+                      "(C port of reference engine.py gemv)", "seconds": round(dt, 2)}
 
 
 def run_reference(args):
@@ -348,7 +376,7 @@ def run_reference(args):
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
-    ls = _oracle_layer_set(99, SHAPES)
+    ls = _oracle_layer_set(99)
     for _ in range(min(args.warmup, 1)):
         _oracle_step(ls, threads)
     steps = max(1, min(args.steps, 3))  # bounded: each step is seconds of CPU work
@@ -356,13 +384,13 @@ def run_reference(args):
     for _ in range(steps):
         _oracle_step(ls, threads)
     dt = (time.perf_counter() - t0) / steps
-    v = round(step_bytes(SHAPES) / dt / 1e9, 4)
+    v = round(step_bytes() / dt / 1e9, 4)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s",
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32 (fp16 tables, fp32 accumulate)", "data": "synthetic random-init",
-        "config": {"workload": "llama2-7b decode layer set", "bits": BITS, "batch": 1},
+        "config": {"workload": "llama2-7b decode layer set (configs[1])", "bits": BITS, "batch": 1},
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": f"{steps} full step(s), {threads} threads, oracle/anyprec_oracle.c "
                                    "(C port of the reference engine.py pipeline)"},
@@ -373,7 +401,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     args = ap.parse_args()

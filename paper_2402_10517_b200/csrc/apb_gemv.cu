@@ -59,10 +59,14 @@ __device__ unsigned long long* g_timeline = nullptr;
             g_timeline[(size_t)blockIdx.x * 8 + (i)] = t_;                 \
         }                                                                  \
     } while (0)
+// per-warp cycle accounting: [prologue, in-unit, total, units]
+__device__ unsigned long long* g_warpstat = nullptr;
+#define APB_CLK(v) long long v = clock64()
 #else
 #define APB_TS(i) \
     do {          \
     } while (0)
+#define APB_CLK(v)
 #endif
 
 struct GemvProblem {
@@ -239,6 +243,10 @@ __global__ void __launch_bounds__(GemvBounds<NG>::kThreads, GemvBounds<NG>::kMin
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, q = lane & 3;
     const int nthreads = blockDim.x;
+    APB_CLK(clk_start);
+#ifdef APB_TIMELINE
+    long long clk_units = 0, n_units_done = 0, clk_main = 0;
+#endif
     if ((uint32_t)__cvta_generic_to_shared(smem) != APB_SMEM_BASE) __trap();  // see lds_table
 
     // contiguous cost-balanced item range of this CTA
@@ -394,6 +402,10 @@ __global__ void __launch_bounds__(GemvBounds<NG>::kThreads, GemvBounds<NG>::kMin
     }
     __syncthreads();
     APB_TS(3);
+    APB_CLK(clk_main0);
+#ifdef APB_TIMELINE
+    clk_main = clk_main0;
+#endif
 
     const uint32_t off0 = (uint32_t)lane * 4u, off1 = 128u + (uint32_t)lane * 4u;
     const int m_out = L.x_split ? (L.m_x >> 1) : L.m_x;
@@ -471,6 +483,7 @@ __global__ void __launch_bounds__(GemvBounds<NG>::kThreads, GemvBounds<NG>::kMin
 
         // ---- this warp's units; the buffer just consumed is refilled with the
         //      unit two steps ahead (possibly of the next item)
+        APB_CLK(clk_u0);
 #pragma unroll 1
         for (int u = warp; u < n_units; u += kWarps) {
             if (j & 1) {
@@ -481,7 +494,13 @@ __global__ void __launch_bounds__(GemvBounds<NG>::kThreads, GemvBounds<NG>::kMin
                 li_load(bufA);
             }
             ++j;
+#ifdef APB_TIMELINE
+            ++n_units_done;
+#endif
         }
+#ifdef APB_TIMELINE
+        clk_units += clock64() - clk_u0;
+#endif
 
         // ---- item boundary: fixed-order reduction + next table ---------------
 #pragma unroll
@@ -532,6 +551,15 @@ __global__ void __launch_bounds__(GemvBounds<NG>::kThreads, GemvBounds<NG>::kMin
         __syncthreads();  // S2
     }
     APB_TS(5);
+#ifdef APB_TIMELINE
+    if (lane == 0 && g_warpstat) {
+        unsigned long long* w = g_warpstat + ((size_t)blockIdx.x * kWarps + warp) * 4;
+        w[0] = clk_main - clk_start;
+        w[1] = clk_units;
+        w[2] = clock64() - clk_start;
+        w[3] = n_units_done;
+    }
+#endif
 }
 
 template <int K, int NG>
@@ -705,6 +733,9 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
 #ifdef APB_TIMELINE
 extern "C" int apb_debug_set_timeline(unsigned long long* p) {
     return cudaMemcpyToSymbol(g_timeline, &p, sizeof(p)) == cudaSuccess ? APB_OK : APB_ERR_CUDA;
+}
+extern "C" int apb_debug_set_warpstat(unsigned long long* p) {
+    return cudaMemcpyToSymbol(g_warpstat, &p, sizeof(p)) == cudaSuccess ? APB_OK : APB_ERR_CUDA;
 }
 #endif
 

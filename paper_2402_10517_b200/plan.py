@@ -32,7 +32,7 @@ def _ldx(cols: int) -> int:
 
 class GemvPlan:
     def __init__(self, preps, k: int, m: int = 1, grouped: bool = True, x_split: bool = False,
-                 y_fp16: bool = False, pdl: bool = False):
+                 y_fp16: bool = False, pdl: bool = False, shared_x: bool = False):
         torch = dev.require_cuda()
         for p in preps:
             if k not in p.tables16:
@@ -48,8 +48,15 @@ class GemvPlan:
         # are never written by the kernels that precede it in a decode loop
         self.flags = APB_FLAG_PDL if pdl else 0
         ydt = torch.float16 if y_fp16 else torch.float32
-        self.x = [torch.zeros((self.m_x, _ldx(p.tensor.cols)), dtype=torch.float16, device="cuda")
-                  for p in self.preps]
+        if shared_x:  # one activation for every layer (e.g. q/k/v, gate/up)
+            cols = {p.tensor.cols for p in self.preps}
+            if len(cols) != 1:
+                raise ParameterError("shared_x needs layers with equal in_features")
+            x0 = torch.zeros((self.m_x, _ldx(cols.pop())), dtype=torch.float16, device="cuda")
+            self.x = [x0] * len(self.preps)
+        else:
+            self.x = [torch.zeros((self.m_x, _ldx(p.tensor.cols)), dtype=torch.float16, device="cuda")
+                      for p in self.preps]
         self.y = [torch.zeros((m, p.tensor.rows), dtype=ydt, device="cuda") for p in self.preps]
         ts = [p.tensor for p in self.preps]
         n = len(ts)
