@@ -212,9 +212,12 @@ def run_ours(args):
     torch.cuda.synchronize()
     graph = None
     try:
+        if args.profile:
+            raise RuntimeError("--profile: eager launches")
         graph, _ = time_graph(torch, step, 1)
     except Exception as e:  # NCCL capture not available: eager launches
-        print(f"[bench] CUDA graph capture failed ({e}); timing eager launches", file=sys.stderr)
+        if not args.profile:
+            print(f"[bench] CUDA graph capture failed ({e}); timing eager launches", file=sys.stderr)
         graph = None
     for _ in range(args.warmup):
         graph.replay() if graph is not None else step()
@@ -264,6 +267,10 @@ def run_ours(args):
                              "(every launch in it is the GEMV kernel)"},
         "clocks": clocks,
     }
+    if args.profile:
+        if rank == 0:
+            print(json.dumps(result))
+        return
     if world == 1:
         result["per_gemv_us"] = per_gemv_detail(torch, plan, copies)
         result["grouped_all7_GBps"] = grouped_all7(torch, plan, copies)
@@ -404,6 +411,8 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--profile", action="store_true",
+                    help="profiling run (under ncu): eager launches, skip detail/e2e/CPU legs")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -43,10 +43,6 @@ namespace apb {
 
 constexpr int kMaxGroup = 16;
 constexpr int kRowsPerCta = 16;
-#ifndef APB_WARPS
-#define APB_WARPS 8
-#endif
-constexpr int kWarps = APB_WARPS;
 
 #ifdef APB_TIMELINE
 // Debug builds (tools/timeline): per-CTA phase timestamps (globaltimer, ns).
@@ -175,7 +171,7 @@ __device__ __forceinline__ void decode_word(const uint32_t* Q, uint32_t off, uin
         for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int p = 0; p < 4; ++p)
-                out[p * 4 + j] = lds_table(prmt(U[j], off, 0x5504u | (uint32_t)(p << 4)));
+                out[p * 4 + j] = lds_table(prmt(U[j], off, 0x7604u | (uint32_t)(p << 4)));
     } else {
         uint32_t Wb[8];
         to_bytes<K>(Q, Wb);
@@ -183,7 +179,7 @@ __device__ __forceinline__ void decode_word(const uint32_t* Q, uint32_t off, uin
         for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
-                const uint32_t sel = 0x5504u | (uint32_t)(p << 4);
+                const uint32_t sel = 0x7604u | (uint32_t)(p << 4);
                 const uint32_t e = lds_table(prmt(Wb[2 * j], off, sel));
                 const uint32_t o = lds_table(prmt(Wb[2 * j + 1], off, sel));
                 out[p * 4 + j] = e + (o << 16);  // IMAD: o * 65536 + e (e < 65536)
@@ -191,12 +187,42 @@ __device__ __forceinline__ void decode_word(const uint32_t* Q, uint32_t off, uin
     }
 }
 
-template <int NG>
-struct GemvBounds {
-    // NG == 1: <= 128 registers so 16 warps (two 256-thread CTAs) are resident per SM.
-    static constexpr int kThreads = kWarps * 32;
-    static constexpr int kMinBlocks = NG == 1 ? 16 / kWarps : 8 / kWarps;
+// ---- warp-specialised persistent kernel --------------------------------------
+// One CTA per SM.  Compute warps stream units (decode + MMA) continuously
+// across row blocks; service warps (1 or 2, by table size) build each block's
+// lookup table into one of two table slots, stage activations, and reduce +
+// store each block's outputs.  Compute and service warps hand off through
+// mbarriers (table_ready[slot], item_done[slot]); there is no CTA-wide barrier
+// in the steady state, so a slow warp never stalls the others.
+template <int K, int NG>
+struct WsGeom {
+    static constexpr int kTotalWarps = NG == 1 ? 16 : 8;
+    static constexpr int kServiceWarps = TableGeom<K>::kEntries >= 256 ? 2 : 1;
+    static constexpr int kComputeWarps = kTotalWarps - kServiceWarps;
+    static constexpr int kThreads = kTotalWarps * 32;
+    // table slot 1 sits 64 KB after slot 0, so the slot index is address byte 2
+    // and the lookup address stays one PRMT (see decode_word / lds_table)
+    static constexpr int kSlotStride = 64 * 1024;
+    static constexpr int kRedBytes = kComputeWarps * kRowsPerCta * 8 * NG * 4;  // one slot
 };
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
 
 __device__ __forceinline__ int problem_of(const GemvLaunch& L, int item) {
     int pi = 0;
@@ -205,16 +231,19 @@ __device__ __forceinline__ int problem_of(const GemvLaunch& L, int item) {
         if (item >= L.prob[i].item_begin) pi = i;
     return pi;
 }
+__device__ __forceinline__ int problem_end(const GemvLaunch& L, int pi) {
+    return pi + 1 < L.n_prob ? L.prob[pi + 1].item_begin : L.n_items;
+}
 
 // First item whose cumulative cost start is >= target (items are cost-uniform
-// within a problem, cost = n_tiles).  Used to give every CTA a contiguous,
+// within a problem, cost = n_tiles).  Every CTA gets a contiguous,
 // cost-balanced item range.
 __device__ __forceinline__ int item_at_cost(const GemvLaunch& L, int64_t target) {
     if (target >= L.total_cost) return L.n_items;
 #pragma unroll 1
     for (int i = 0; i < L.n_prob; ++i) {
         const GemvProblem& P = L.prob[i];
-        const int n = (i + 1 < L.n_prob ? L.prob[i + 1].item_begin : L.n_items) - P.item_begin;
+        const int n = problem_end(L, i) - P.item_begin;
         const int64_t end = P.cost_begin + (int64_t)n * P.n_tiles;
         if (target < end) {
             const int64_t d = target - P.cost_begin;
@@ -224,211 +253,284 @@ __device__ __forceinline__ int item_at_cost(const GemvLaunch& L, int64_t target)
     return L.n_items;
 }
 
+// smem layout: [table slot 0][.. slot 1 at +64K][red x2][xs x2][mbarriers]
+template <int K, int NG>
+struct WsLayout {
+    static constexpr int kTable1 = WsGeom<K, NG>::kSlotStride;
+    static constexpr int kRed = kTable1 + TableGeom<K>::kBytes;
+    static constexpr int kXs = kRed + 2 * WsGeom<K, NG>::kRedBytes;
+    __host__ __device__ static size_t bars(int64_t xs_bytes) { return (size_t)kXs + 2 * (size_t)((xs_bytes + 127) / 128 * 128); }
+    __host__ __device__ static size_t total(int64_t xs_bytes) { return bars(xs_bytes) + 64; }
+};
+
 template <int K, int NG, int UB, bool XS>
-__global__ void __launch_bounds__(GemvBounds<NG>::kThreads, GemvBounds<NG>::kMinBlocks)
+__global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
     gemv_kernel(const __grid_constant__ GemvLaunch L) {
     using V = UnitVec<UB>;
     using VT = typename V::T;
     using TG = TableGeom<K>;
+    using G = WsGeom<K, NG>;
+    using LY = WsLayout<K, NG>;
+    constexpr int WC = G::kComputeWarps;
     constexpr int WPU = UB / 4;          // lane words per unit per row
     constexpr int UPT = 128 / (4 * UB);  // units per tile
     constexpr int RC = 8 * NG;           // reduction columns
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* const table = smem;                      // [TB]
-    uint8_t* const stage = smem + TG::kBytes;         // [16 rows][2^K] fp16 (next item)
-    float* const red = reinterpret_cast<float*>(stage + TG::kStageBytes);  // [W][16][RC]
-    uint8_t* const xs = reinterpret_cast<uint8_t*>(red + kWarps * kRowsPerCta * RC);
-
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, q = lane & 3;
-    const int nthreads = blockDim.x;
-    APB_CLK(clk_start);
-#ifdef APB_TIMELINE
-    long long clk_units = 0, n_units_done = 0, clk_main = 0;
-#endif
-    if ((uint32_t)__cvta_generic_to_shared(smem) != APB_SMEM_BASE) __trap();  // see lds_table
+    if (smem_addr(smem) != APB_SMEM_BASE) __trap();  // see lds_table
 
-    // contiguous cost-balanced item range of this CTA
     const int first = item_at_cost(L, L.total_cost * (int64_t)blockIdx.x / gridDim.x);
     const int last = item_at_cost(L, L.total_cost * (int64_t)(blockIdx.x + 1) / gridDim.x);
-    APB_TS(0);
     asm volatile("griddepcontrol.launch_dependents;");
     if (first >= last) return;
+    const int n_local = last - first;
 
-    // ---- plane-load iterator: walks this warp's units across the item range.
-    // Items are contiguous and problems only advance, so everything is
-    // incremental (no search, no 64-bit multiply per unit).
-    int li_item = first, li_u = warp;
-    int li_pi = problem_of(L, first);
-    int li_pend = 0, li_units = 0;  // first item of the next problem; units per item
-    int64_t li_rows = 0, li_rb_bytes = 0, li_row0 = 0, li_pstride = 0;
+    float* const red = reinterpret_cast<float*>(smem + LY::kRed);  // [2][WC][16][RC]
+    const int64_t xs_slot = (L.xs_bytes + 127) / 128 * 128;
+    uint8_t* const xs = smem + LY::kXs;                              // [2][xs_slot]
+    const uint32_t bar = smem_addr(smem + LY::bars(L.xs_bytes));
+    // bar + 0 / 8: table_ready[slot] (count = service warps)
+    // bar + 16 / 24: item_done[slot] (count = compute warps)
+    if (tid == 0) {
+        mbar_init(bar + 0, G::kServiceWarps);
+        mbar_init(bar + 8, G::kServiceWarps);
+        mbar_init(bar + 16, WC);
+        mbar_init(bar + 24, WC);
+    }
+    __syncthreads();
+
+    if (warp >= WC) {
+        // =============================== service warps =========================
+        const int nst = G::kServiceWarps * 32, st = tid - WC * 32;
+        // centroid rows of the next block, prefetched into registers
+        constexpr int kItems = TG::kPair ? (kRowsPerCta << K) : (kRowsPerCta * (1 << K) / 8);
+        constexpr int kPer = (kItems + G::kServiceWarps * 32 - 1) / (G::kServiceWarps * 32);
+        constexpr int kRowVecs = TG::kPair ? ((1 << K) + 7) / 8 : 1;
+        uint4 src[kPer][kRowVecs];
+        auto load_lut = [&](int item, int pi) {
+            const GemvProblem& P = L.prob[pi];
+            const int64_t rb = item - P.item_begin;
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                const int it = st + i * nst;
+                const int rl = it & 15;
+                const int64_t row = rb * kRowsPerCta + rl;
+#pragma unroll
+                for (int v = 0; v < kRowVecs; ++v) src[i][v] = make_uint4(0, 0, 0, 0);
+                if (it < kItems && row < P.rows) {
+                    const uint16_t* lr = P.lut + row * (1 << K);
+                    if constexpr (TG::kPair) {
+                        if constexpr ((1 << K) >= 8) {
+#pragma unroll
+                            for (int v = 0; v < kRowVecs; ++v)
+                                src[i][v] = __ldg(reinterpret_cast<const uint4*>(lr) + v);
+                        } else {
+                            const uint2 h = __ldg(reinterpret_cast<const uint2*>(lr));
+                            src[i][0] = make_uint4(h.x, h.y, 0, 0);
+                        }
+                    } else {
+                        src[i][0] = __ldg(reinterpret_cast<const uint4*>(lr) + (it >> 4));
+                    }
+                }
+            }
+        };
+        auto half_at = [&](const uint4(&rv)[kRowVecs], int i) -> uint32_t {
+            const uint32_t w = u4_word(rv[i >> 3], (i >> 1) & 3);
+            return (i & 1) ? (w >> 16) : (w & 0xFFFFu);
+        };
+        auto build = [&](int slot) {
+            uint8_t* const tbase = smem + slot * G::kSlotStride;
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                const int it = st + i * nst;
+                if (it >= kItems) continue;
+                const int rl = it & 15;
+                uint8_t* dst = tbase + rl * 16;
+                if constexpr (TG::kPair) {
+                    const int ce = it >> 4;  // its 2^K entries are (L[ce], L[co]) for every co
+                    uint32_t lce = 0;
+#pragma unroll
+                    for (int c = 0; c < (1 << K); ++c)
+                        if (c == ce) lce = half_at(src[i], c);
+                    uint32_t sce = 0;  // code bit b -> pair-index bit 2b
+#pragma unroll
+                    for (int b = 0; b < K; ++b) sce |= (((uint32_t)ce >> b) & 1u) << (2 * b);
+#pragma unroll
+                    for (int co = 0; co < (1 << K); ++co) {
+                        uint32_t sco = 0;
+#pragma unroll
+                        for (int b = 0; b < K; ++b) sco |= ((uint32_t)(co >> b) & 1u) << (2 * b + 1);
+                        const uint32_t v = lce | (half_at(src[i], co) << 16);
+                        *reinterpret_cast<uint4*>(dst + (sce | sco) * 256) = make_uint4(v, v, v, v);
+                    }
+                } else {
+                    const int e8 = it >> 4;
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) {
+                        const uint32_t v = half_at(src[i], jj);
+                        *reinterpret_cast<uint4*>(dst + (e8 * 8 + jj) * 256) = make_uint4(v, v, v, v);
+                    }
+                }
+            }
+        };
+        auto stage_x = [&](int pi, int xb) {
+            const GemvProblem& P = L.prob[pi];
+            const int64_t padded = (int64_t)P.n_tiles * kTileWeights;
+            const int chunks = (int)(padded / 8);
+            for (int m = 0; m < L.m_x; ++m) {
+                const uint16_t* srow = P.x + (int64_t)m * P.ldx;
+                uint8_t* drow = xs + xb * xs_slot + (int64_t)m * padded * 2;
+                for (int c = st; c < chunks; c += nst) {
+                    const int64_t col = (int64_t)c * 8;
+                    const int64_t nb = (P.cols - col) * 2;
+                    cp_async16(drow + col * 2, nb > 0 ? (const void*)(srow + col) : (const void*)srow,
+                               nb >= 16 ? 16 : (nb > 0 ? (int)nb : 0));
+                }
+            }
+            cp_async_commit();
+            cp_async_wait_all();
+        };
+        auto reduce = [&](int item, int pi, int slot) {
+            const GemvProblem& P = L.prob[pi];
+            const int64_t rb = item - P.item_begin;
+            const int m_out = L.x_split ? (L.m_x >> 1) : L.m_x;
+            const float* r = red + slot * (WC * kRowsPerCta * RC);
+            for (int i = st; i < kRowsPerCta * m_out; i += nst) {
+                const int rl = i & 15, m = i >> 4;
+                const int64_t row = rb * kRowsPerCta + rl;
+                if (row >= P.rows) continue;
+                float sum;
+                if (L.x_split) {
+                    float hi = 0.f, lo = 0.f;
+#pragma unroll
+                    for (int w = 0; w < WC; ++w) hi += r[(w * kRowsPerCta + rl) * RC + 2 * m];
+#pragma unroll
+                    for (int w = 0; w < WC; ++w) lo += r[(w * kRowsPerCta + rl) * RC + 2 * m + 1];
+                    sum = hi + lo;
+                } else {
+                    sum = 0.f;
+#pragma unroll
+                    for (int w = 0; w < WC; ++w) sum += r[(w * kRowsPerCta + rl) * RC + m];
+                }
+                if (L.y_f16)
+                    reinterpret_cast<__half*>(P.y)[(int64_t)m * P.ldy + row] = __float2half_rn(sum);
+                else
+                    reinterpret_cast<float*>(P.y)[(int64_t)m * P.ldy + row] = sum;
+            }
+        };
+
+        // activations / outputs may belong to the previous kernel in the stream
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        int pi = problem_of(L, first), pend = problem_end(L, pi);
+        int xb = 0, pi_hist[2] = {pi, pi};
+        load_lut(first, pi);
+#pragma unroll 1
+        for (int jl = 0; jl < n_local + 2; ++jl) {
+            if (jl >= 2) {  // block jl-2 finished by every compute warp: reduce it, free its slot
+                mbar_wait(bar + 16 + 8 * (jl & 1), ((jl - 2) >> 1) & 1);
+                reduce(first + jl - 2, pi_hist[jl & 1], jl & 1);
+            }
+            if (jl < n_local) {
+                const int item = first + jl;
+                if (item >= pend) {  // next layer of a grouped launch
+                    pi = problem_of(L, item);
+                    pend = problem_end(L, pi);
+                    xb ^= 1;
+                    if constexpr (XS) stage_x(pi, xb);
+                } else if (jl == 0) {
+                    if constexpr (XS) stage_x(pi, xb);
+                }
+                pi_hist[jl & 1] = pi;
+                build(jl & 1);
+                // prefetch the next block's centroid rows while this one is consumed
+                if (item + 1 < last) {
+                    const int npi = item + 1 >= pend ? problem_of(L, item + 1) : pi;
+                    load_lut(item + 1, npi);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar + 8 * (jl & 1));
+            }
+        }
+        return;
+    }
+
+    // =============================== compute warps =============================
+    if constexpr (!XS) asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int w = warp;
+    // plane-load iterator over this warp's global unit sequence w, w+WC, ...
+    int li_j = 0, li_pi = problem_of(L, first), li_pend = problem_end(L, li_pi);
+    int64_t li_base = 0;
+    int li_units = 0;
+    int64_t li_rows = 0, li_rbytes = 0, li_row0 = 0, li_pstride = 0;
     const uint8_t* li_b0 = nullptr;
-    auto li_problem = [&]() {  // cache the fields of problem li_pi at item li_item
+    int64_t li_g = w;
+    auto li_fields = [&](int item) {
         const GemvProblem& P = L.prob[li_pi];
-        li_pend = li_pi + 1 < L.n_prob ? L.prob[li_pi + 1].item_begin : L.n_items;
         li_units = P.n_tiles * UPT;
         li_rows = P.rows;
-        li_rb_bytes = P.row_bytes;
+        li_rbytes = P.row_bytes;
         li_pstride = P.plane_stride;
-        li_row0 = (int64_t)(li_item - P.item_begin) * kRowsPerCta + g;
+        li_row0 = (int64_t)(item - P.item_begin) * kRowsPerCta + g;
         li_b0 = P.planes + li_row0 * P.row_bytes + q * UB;
     };
-    auto li_skip_empty = [&]() {  // skip problems whose items have no unit for this warp
-        while (li_item < last && li_u >= li_units) {
-            li_item = li_pend;
-            if (li_item >= last) break;
-            ++li_pi;
-            li_problem();
-        }
-    };
+    li_fields(first);
     auto li_load = [&](VT(&dst)[2][K]) {
-        if (li_item >= last) return;
-        const int tile = li_u / UPT, s = li_u - tile * UPT;
+        while (li_j < n_local && li_g >= li_base + li_units) {  // advance to the unit's block
+            li_base += li_units;
+            ++li_j;
+            if (li_j >= n_local) break;
+            const int item = first + li_j;
+            if (item >= li_pend) {
+                ++li_pi;
+                while (item >= problem_end(L, li_pi)) ++li_pi;
+                li_pend = problem_end(L, li_pi);
+                li_fields(item);
+            } else {
+                li_row0 += kRowsPerCta;
+                li_b0 += kRowsPerCta * li_rbytes;
+            }
+        }
+        if (li_j >= n_local) return;
+        const int u = (int)(li_g - li_base);
+        const int tile = u / UPT, s = u - tile * UPT;
         const uint8_t* p0 = li_b0 + (int64_t)tile * kTileBytes + s * 4 * UB;
-        const uint8_t* p1 = p0 + 8 * li_rb_bytes;
+        const uint8_t* p1 = p0 + 8 * li_rbytes;
         const bool ok0 = li_row0 < li_rows, ok1 = li_row0 + 8 < li_rows;
 #pragma unroll
         for (int p = 0; p < K; ++p) {
             dst[0][K - 1 - p] = ok0 ? V::load(p0 + p * li_pstride) : V::zero();
             dst[1][K - 1 - p] = ok1 ? V::load(p1 + p * li_pstride) : V::zero();
         }
-        li_u += kWarps;
-        if (li_u >= li_units) {  // next item
-            li_u = warp;
-            ++li_item;
-            if (li_item < last) {
-                if (li_item >= li_pend) {
-                    ++li_pi;
-                    li_problem();
-                    li_skip_empty();
-                } else {
-                    li_row0 += kRowsPerCta;
-                    li_b0 += kRowsPerCta * li_rb_bytes;
-                }
-            }
-        }
+        li_g += WC;
     };
 
-    // centroid rows of an item -> stage (cp.async, zero-filled past the last row)
-    auto stage_lut = [&](int item, int pi) {
-        const GemvProblem& P = L.prob[pi];
-        const int64_t rb = item - P.item_begin;
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.lut) + rb * TG::kStageBytes;
-        const int64_t valid = (P.rows - rb * kRowsPerCta) * (int64_t)(2 << K);  // bytes
-        for (int c = tid; c < TG::kStageBytes / 16; c += nthreads) {
-            const int64_t o = (int64_t)c * 16;
-            const int64_t nb = valid - o;
-            cp_async16(stage + o, nb > 0 ? (const void*)(src + o) : (const void*)src,
-                       nb >= 16 ? 16 : (nb > 0 ? (int)nb : 0));
-        }
-    };
-    // replicated lookup tables from the staged centroid rows
-    auto build_table = [&]() {
-        const uint16_t* st = reinterpret_cast<const uint16_t*>(stage);
-        if constexpr (TG::kPair) {
-            // item (rl, ce): the 2^K entries (L[ce], L[co]) for every co
-            for (int it = tid; it < (kRowsPerCta << K); it += nthreads) {
-                const int rl = it & 15, ce = it >> 4;
-                const uint16_t* lr = st + (rl << K);
-                const uint32_t lce = lr[ce];
-                uint32_t sce = 0;  // code bit i -> pair-index bit 2i
-#pragma unroll
-                for (int i = 0; i < K; ++i) sce |= (((uint32_t)ce >> i) & 1u) << (2 * i);
-                uint8_t* dst = table + rl * 16 + sce * 256;
-#pragma unroll
-                for (int co = 0; co < (1 << K); ++co) {
-                    uint32_t sco = 0;
-#pragma unroll
-                    for (int i = 0; i < K; ++i) sco |= ((uint32_t)(co >> i) & 1u) << (2 * i + 1);
-                    const uint32_t v = lce | ((uint32_t)lr[co] << 16);
-                    *reinterpret_cast<uint4*>(dst + sco * 256) = make_uint4(v, v, v, v);
-                }
-            }
-        } else {
-            // item (rl, 8 consecutive entries)
-            for (int it = tid; it < kRowsPerCta * (1 << K) / 8; it += nthreads) {
-                const int rl = it & 15, e8 = it >> 4;
-                const uint4 h = lds128(stage + (rl << K) * 2 + e8 * 16);
-                uint8_t* dst = table + rl * 16 + e8 * 8 * 256;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t w = u4_word(h, j >> 1);
-                    const uint32_t v = (j & 1) ? (w >> 16) : (w & 0xFFFFu);
-                    *reinterpret_cast<uint4*>(dst + j * 256) = make_uint4(v, v, v, v);
-                }
-            }
-        }
-    };
-    // activations of a problem -> xs ([m_x][padded] fp16, zero beyond cols)
-    auto stage_x = [&](int pi) {
-        const GemvProblem& P = L.prob[pi];
-        const int64_t padded = (int64_t)P.n_tiles * kTileWeights;
-        const int chunks = (int)(padded / 8);
-        for (int m = 0; m < L.m_x; ++m) {
-            const uint16_t* srow = P.x + (int64_t)m * P.ldx;
-            uint8_t* drow = xs + (int64_t)m * padded * 2;
-            for (int c = tid; c < chunks; c += nthreads) {
-                const int64_t col = (int64_t)c * 8;
-                const int64_t nb = (P.cols - col) * 2;
-                cp_async16(drow + col * 2, nb > 0 ? (const void*)(srow + col) : (const void*)srow,
-                           nb >= 16 ? 16 : (nb > 0 ? (int)nb : 0));
-            }
-        }
-    };
-
-    // ---- prologue --------------------------------------------------------------
-    int cur_pi = li_pi;
-    stage_lut(first, cur_pi);
-    cp_async_commit();
     VT bufA[2][K], bufB[2][K];
-    li_problem();
-    li_skip_empty();
     li_load(bufA);
     li_load(bufB);
-    APB_TS(1);
-    cp_async_wait_all();
-    __syncthreads();
-    build_table();
-    APB_TS(2);
-    // Programmatic dependent launch: everything above touches only weights
-    // (planes, tables); activations may come from the previous kernel in the
-    // stream, so wait for it here (no-op without PDL).
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if constexpr (XS) {
-        stage_x(cur_pi);
-        cp_async_commit();
-        cp_async_wait_all();
-    }
-    __syncthreads();
-    APB_TS(3);
-    APB_CLK(clk_main0);
-#ifdef APB_TIMELINE
-    clk_main = clk_main0;
-#endif
 
-    const uint32_t off0 = (uint32_t)lane * 4u, off1 = 128u + (uint32_t)lane * 4u;
-    const int m_out = L.x_split ? (L.m_x >> 1) : L.m_x;
-    int j = 0;  // ring position (A/B)
-
+    int xm[NG];
+#pragma unroll
+    for (int ng = 0; ng < NG; ++ng) xm[ng] = min(g + 8 * ng, L.m_x - 1);
+    int cpi = problem_of(L, first), cpend = problem_end(L, cpi), xb = 0;
+    int64_t base = 0, gu = w;
+    int ring = 0;
 #pragma unroll 1
-    for (int item = first; item < last; ++item) {
-        const GemvProblem& P = L.prob[cur_pi];
-        const int64_t rb = item - P.item_begin;
-        const int n_units = P.n_tiles * UPT;
+    for (int jl = 0; jl < n_local; ++jl) {
+        const int item = first + jl;
+        if (item >= cpend) {
+            cpi = problem_of(L, item);
+            cpend = problem_end(L, cpi);
+            xb ^= 1;
+        }
+        const GemvProblem& P = L.prob[cpi];
+        const int units = P.n_tiles * UPT;
         const int64_t cols = P.cols;
         const int64_t padded = (int64_t)P.n_tiles * kTileWeights;
-        const int nxt = item + 1;
-        const int cur_pend = cur_pi + 1 < L.n_prob ? L.prob[cur_pi + 1].item_begin : L.n_items;
-        const int nxt_pi = (nxt < last && nxt >= cur_pend) ? cur_pi + 1 : cur_pi;
-        // next block's centroid rows land in `stage` while this block computes
-        if (nxt < last) stage_lut(nxt, nxt_pi);
-        cp_async_commit();
-
-        int xm[NG];
-#pragma unroll
-        for (int ng = 0; ng < NG; ++ng) xm[ng] = min(g + 8 * ng, L.m_x - 1);
-        // two independent accumulator chains (even / odd 256-column run)
+        const uint8_t* const xsb = xs + xb * xs_slot;
+        const uint32_t slot_bits = (uint32_t)(jl & 1) << 16;
+        const uint32_t off0 = slot_bits | ((uint32_t)lane * 4u), off1 = off0 + 128u;
         float acc[NG][2][4];
 #pragma unroll
         for (int ng = 0; ng < NG; ++ng)
@@ -439,21 +541,20 @@ __global__ void __launch_bounds__(GemvBounds<NG>::kThreads, GemvBounds<NG>::kMin
             const int tile = uu / UPT, s = uu - tile * UPT;
             const bool full_tile = XS || (int64_t)(tile + 1) * kTileWeights <= cols;
 #pragma unroll
-            for (int w = 0; w < WPU; ++w) {
-                const int t = s * UB + q * WPU + w;  // lane word within the tile
+            for (int wi = 0; wi < WPU; ++wi) {
+                const int t = s * UB + q * WPU + wi;  // lane word within the tile
                 const int64_t colbase = (int64_t)tile * kTileWeights + 8 * t;
                 uint4 xv[NG][4];
 #pragma unroll
                 for (int ng = 0; ng < NG; ++ng)
 #pragma unroll
                     for (int p = 0; p < 4; ++p) {
-                        if constexpr (XS) {
-                            // only lanes holding a real batch column load x (the
-                            // B columns n >= m_x are never read back): with
-                            // m_x <= 2 that is one shared-memory wavefront, not 4
-                            xv[ng][p] = (g + 8 * ng < L.m_x)
-                                            ? lds128(xs + (xm[ng] * padded + colbase + 256 * p) * 2)
-                                            : make_uint4(0, 0, 0, 0);
+                        // only lanes holding a real batch column load x (B columns
+                        // n >= m_x are never read back)
+                        if (g + 8 * ng >= L.m_x) {
+                            xv[ng][p] = make_uint4(0, 0, 0, 0);
+                        } else if constexpr (XS) {
+                            xv[ng][p] = lds128(xsb + (xm[ng] * padded + colbase + 256 * p) * 2);
                         } else {
                             const uint16_t* xr = P.x + (int64_t)xm[ng] * P.ldx;
                             xv[ng][p] = full_tile ? __ldg(reinterpret_cast<const uint4*>(xr + colbase + 256 * p))
@@ -463,8 +564,8 @@ __global__ void __launch_bounds__(GemvBounds<NG>::kThreads, GemvBounds<NG>::kMin
                 uint32_t Q0[K], Q1[K];
 #pragma unroll
                 for (int i = 0; i < K; ++i) {
-                    Q0[i] = V::word(buf[0][i], w);
-                    Q1[i] = V::word(buf[1][i], w);
+                    Q0[i] = V::word(buf[0][i], wi);
+                    Q1[i] = V::word(buf[1][i], wi);
                 }
                 uint32_t a0[16], a1[16];
                 decode_word<K>(Q0, off0, a0);
@@ -481,94 +582,37 @@ __global__ void __launch_bounds__(GemvBounds<NG>::kThreads, GemvBounds<NG>::kMin
             }
         };
 
-        // ---- this warp's units; the buffer just consumed is refilled with the
-        //      unit two steps ahead (possibly of the next item)
-        APB_CLK(clk_u0);
+        mbar_wait(bar + 8 * (jl & 1), (jl >> 1) & 1);  // this block's table (and x) ready
 #pragma unroll 1
-        for (int u = warp; u < n_units; u += kWarps) {
-            if (j & 1) {
+        for (; gu < base + units; gu += WC) {
+            const int u = (int)(gu - base);
+            if (ring & 1) {
                 compute_unit(u, bufB);
                 li_load(bufB);
             } else {
                 compute_unit(u, bufA);
                 li_load(bufA);
             }
-            ++j;
-#ifdef APB_TIMELINE
-            ++n_units_done;
-#endif
+            ++ring;
         }
-#ifdef APB_TIMELINE
-        clk_units += clock64() - clk_u0;
-#endif
-
-        // ---- item boundary: fixed-order reduction + next table ---------------
+        float* r = red + (jl & 1) * (WC * kRowsPerCta * RC);
 #pragma unroll
         for (int ng = 0; ng < NG; ++ng) {
-            float* r0p = red + (warp * kRowsPerCta + g) * RC + ng * 8 + 2 * q;
-            float* r1p = red + (warp * kRowsPerCta + g + 8) * RC + ng * 8 + 2 * q;
+            float* r0p = r + (w * kRowsPerCta + g) * RC + ng * 8 + 2 * q;
+            float* r1p = r + (w * kRowsPerCta + g + 8) * RC + ng * 8 + 2 * q;
             r0p[0] = acc[ng][0][0] + acc[ng][1][0];
             r0p[1] = acc[ng][0][1] + acc[ng][1][1];
             r1p[0] = acc[ng][0][2] + acc[ng][1][2];
             r1p[1] = acc[ng][0][3] + acc[ng][1][3];
         }
-        cp_async_wait_all();  // next block's centroid rows
-        __syncthreads();      // S1: table / xs / red free or complete
-        APB_TS(4);
-        for (int i = tid; i < kRowsPerCta * m_out; i += nthreads) {
-            const int rl = i & 15, m = i >> 4;
-            const int64_t row = rb * kRowsPerCta + rl;
-            if (row >= P.rows) continue;
-            float sum;
-            if (L.x_split) {
-                float hi = 0.f, lo = 0.f;
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w) hi += red[(w * kRowsPerCta + rl) * RC + 2 * m];
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w) lo += red[(w * kRowsPerCta + rl) * RC + 2 * m + 1];
-                sum = hi + lo;
-            } else {
-                sum = 0.f;
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w) sum += red[(w * kRowsPerCta + rl) * RC + m];
-            }
-            if (L.y_f16)
-                reinterpret_cast<__half*>(P.y)[(int64_t)m * P.ldy + row] = __float2half_rn(sum);
-            else
-                reinterpret_cast<float*>(P.y)[(int64_t)m * P.ldy + row] = sum;
-        }
-        if (nxt < last) {
-            build_table();
-            if constexpr (XS) {
-                if (nxt_pi != cur_pi) {  // new layer: restage its activations
-                    stage_x(nxt_pi);
-                    cp_async_commit();
-                    cp_async_wait_all();
-                }
-            }
-        }
-        cur_pi = nxt_pi;
-        __syncthreads();  // S2
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar + 16 + 8 * (jl & 1));
+        base += units;
     }
-    APB_TS(5);
-#ifdef APB_TIMELINE
-    if (lane == 0 && g_warpstat) {
-        unsigned long long* w = g_warpstat + ((size_t)blockIdx.x * kWarps + warp) * 4;
-        w[0] = clk_main - clk_start;
-        w[1] = clk_units;
-        w[2] = clock64() - clk_start;
-        w[3] = n_units_done;
-    }
-#endif
-}
-
-template <int K, int NG>
-static size_t smem_bytes(int64_t xs_bytes) {
-    return (size_t)TableGeom<K>::kBytes + TableGeom<K>::kStageBytes +
-           (size_t)kWarps * kRowsPerCta * 8 * NG * 4 + (size_t)xs_bytes;
 }
 
 constexpr int64_t kMaxXsBytes = 48 * 1024;
+constexpr size_t kSmemLimitBytes = 227 * 1024;
 
 static int sm_count() {
     static int cached[64] = {0};
@@ -584,27 +628,23 @@ static int sm_count() {
 
 template <int K, int NG, int UB, bool XS>
 static int launch_variant(const GemvLaunch& L, cudaStream_t s) {
+    using LY = WsLayout<K, NG>;
     auto kern = gemv_kernel<K, NG, UB, XS>;
     static std::atomic<int> configured{0};
     if (!configured.load(std::memory_order_acquire)) {
-        const size_t max_smem = smem_bytes<K, NG>(XS ? kMaxXsBytes : 0);
+        size_t max_smem = LY::total(XS ? kMaxXsBytes : 0);
+        if (max_smem > kSmemLimitBytes) max_smem = kSmemLimitBytes;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem) != cudaSuccess)
-            return APB_ERR_CUDA;
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 (int)cudaSharedmemCarveoutMaxShared) != cudaSuccess)
             return APB_ERR_CUDA;
         configured.store(1, std::memory_order_release);
     }
-    const size_t smem = smem_bytes<K, NG>(XS ? L.xs_bytes : 0);
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GemvBounds<NG>::kThreads, smem) !=
-            cudaSuccess || per_sm < 1)
-        per_sm = 1;
-    int grid = per_sm * sm_count();
+    const size_t smem = LY::total(XS ? L.xs_bytes : 0);
+    if (smem > kSmemLimitBytes) return APB_ERR_PARAM;
+    int grid = sm_count();
     if (grid > L.n_items) grid = L.n_items;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3((unsigned)GemvBounds<NG>::kThreads);
+    cfg.blockDim = dim3((unsigned)WsGeom<K, NG>::kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -621,16 +661,21 @@ constexpr int unit_bytes() {
     return K <= 3 ? 16 : 8;
 }
 
+constexpr size_t kSmemLimit = 227 * 1024;
+
 template <int K, int NG>
-static int dispatch_xs(const GemvLaunch& L, cudaStream_t s) {
+static int dispatch_xs(GemvLaunch& L, cudaStream_t s) {
     if constexpr (NG == 1) {
-        if (L.xs_bytes > 0) return launch_variant<K, NG, unit_bytes<K>(), true>(L, s);
+        // activations in shared memory when both buffers fit next to the tables
+        if (L.xs_bytes > 0 && L.xs_bytes <= kMaxXsBytes && WsLayout<K, NG>::total(L.xs_bytes) <= kSmemLimit)
+            return launch_variant<K, NG, unit_bytes<K>(), true>(L, s);
     }
+    L.xs_bytes = 0;
     return launch_variant<K, NG, unit_bytes<K>(), false>(L, s);
 }
 
 template <int K>
-static int dispatch_ng(int ng, const GemvLaunch& L, cudaStream_t s) {
+static int dispatch_ng(int ng, GemvLaunch& L, cudaStream_t s) {
     switch (ng) {
         case 1: return dispatch_xs<K, 1>(L, s);
         case 2: return dispatch_xs<K, 2>(L, s);
@@ -680,8 +725,7 @@ static int gemv_launch_chunk(int n, const uint8_t* const* planes, const int64_t*
     L.n_items = items;
     L.total_cost = cost;
     const int ng = m_x <= 8 ? 1 : (m_x <= 16 ? 2 : 4);
-    const int64_t xs = (int64_t)m_x * max_padded * 2;
-    L.xs_bytes = (ng == 1 && xs <= kMaxXsBytes) ? xs : 0;
+    L.xs_bytes = (int64_t)m_x * max_padded * 2;  // per buffer; dispatch decides if it fits
     switch (k) {
         case 2: return dispatch_ng<2>(ng, L, s);
         case 3: return dispatch_ng<3>(ng, L, s);
