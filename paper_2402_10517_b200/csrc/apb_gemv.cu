@@ -457,6 +457,9 @@ __global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
     }
 
     // =============================== compute warps =============================
+#ifdef APB_TIMELINE
+    long long clk_start = clock64(), clk_units = 0, clk_ldwait = 0, clk_tblwait = 0, n_done = 0;
+#endif
     if constexpr (!XS) asm volatile("griddepcontrol.wait;" ::: "memory");
     const int w = warp;
     // plane-load iterator over this warp's global unit sequence w, w+WC, ...
@@ -538,6 +541,17 @@ __global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
             for (int c2 = 0; c2 < 2; ++c2) acc[ng][c2][0] = acc[ng][c2][1] = acc[ng][c2][2] = acc[ng][c2][3] = 0.f;
 
         auto compute_unit = [&](int uu, const VT(&buf)[2][K]) {
+#ifdef APB_TIMELINE
+            {  // diagnostics: force the wait for this unit's plane data here
+                long long t0 = clock64();
+                uint32_t dep = 0;
+#pragma unroll
+                for (int i = 0; i < K; ++i) dep ^= V::word(buf[0][i], 0) ^ V::word(buf[1][i], WPU - 1);
+                asm volatile("" ::"r"(dep));
+                if (dep == 0x9e3779b9u) clk_units += 1;  // keep dep live
+                clk_ldwait += clock64() - t0;
+            }
+#endif
             const int tile = uu / UPT, s = uu - tile * UPT;
             const bool full_tile = XS || (int64_t)(tile + 1) * kTileWeights <= cols;
 #pragma unroll
@@ -582,7 +596,14 @@ __global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
             }
         };
 
+#ifdef APB_TIMELINE
+        long long tw0 = clock64();
+#endif
         mbar_wait(bar + 8 * (jl & 1), (jl >> 1) & 1);  // this block's table (and x) ready
+#ifdef APB_TIMELINE
+        clk_tblwait += clock64() - tw0;
+        long long tu0 = clock64();
+#endif
 #pragma unroll 1
         for (; gu < base + units; gu += WC) {
             const int u = (int)(gu - base);
@@ -594,7 +615,13 @@ __global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
                 li_load(bufA);
             }
             ++ring;
+#ifdef APB_TIMELINE
+            ++n_done;
+#endif
         }
+#ifdef APB_TIMELINE
+        clk_units += clock64() - tu0;
+#endif
         float* r = red + (jl & 1) * (WC * kRowsPerCta * RC);
 #pragma unroll
         for (int ng = 0; ng < NG; ++ng) {
@@ -609,6 +636,16 @@ __global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
         if (lane == 0) mbar_arrive(bar + 16 + 8 * (jl & 1));
         base += units;
     }
+#ifdef APB_TIMELINE
+    if (lane == 0 && g_warpstat) {  // [total, in-unit loop, load wait, table wait, units]
+        unsigned long long* st = g_warpstat + ((size_t)blockIdx.x * 16 + warp) * 8;
+        st[0] = clock64() - clk_start;
+        st[1] = clk_units;
+        st[2] = clk_ldwait;
+        st[3] = clk_tblwait;
+        st[4] = n_done;
+    }
+#endif
 }
 
 constexpr int64_t kMaxXsBytes = 48 * 1024;
