@@ -120,6 +120,14 @@ __device__ __forceinline__ uint32_t lds_table(uint32_t off) {
     return v;
 }
 __device__ __forceinline__ uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
+// 16-byte shared load executed only where pred != 0; elsewhere the outputs are
+// don't-care values (used for MMA B-fragment columns that are never read).
+__device__ __forceinline__ void lds128_pred(uint4& v, uint32_t saddr, uint32_t pred) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t"
+        "@p ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
+        : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+        : "r"(saddr), "r"(pred));
+}
 
 __device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -263,50 +271,24 @@ struct WsLayout {
     __host__ __device__ static size_t total(int64_t xs_bytes) { return bars(xs_bytes) + 64; }
 };
 
-template <int K, int NG, int UB, bool XS>
-__global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
-    gemv_kernel(const __grid_constant__ GemvLaunch L) {
-    using V = UnitVec<UB>;
-    using VT = typename V::T;
+// Service role (1-2 warps): for every item of the CTA's range, build its lookup
+// table into table slot (j & 1), stage the layer's activations (XS) on a layer
+// change, and -- two items later, once every compute warp has arrived on
+// item_done -- reduce the per-warp partials and store y.  Shared by the v5 and
+// v6 kernels.
+template <int K, int NSW, int WC, int RC, bool XS, int XUB = 0, int NSLOT = 2, int KPF = 0>
+__device__ __forceinline__ void service_role(const GemvLaunch& L, int first, int last, uint8_t* smem,
+                                             uint32_t bar, float* red, uint8_t* xs, int64_t xs_slot,
+                                             int st, int slot_stride) {
     using TG = TableGeom<K>;
-    using G = WsGeom<K, NG>;
-    using LY = WsLayout<K, NG>;
-    constexpr int WC = G::kComputeWarps;
-    constexpr int WPU = UB / 4;          // lane words per unit per row
-    constexpr int UPT = 128 / (4 * UB);  // units per tile
-    constexpr int RC = 8 * NG;           // reduction columns
-
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int g = lane >> 2, q = lane & 3;
-    if (smem_addr(smem) != APB_SMEM_BASE) __trap();  // see lds_table
-
-    const int first = item_at_cost(L, L.total_cost * (int64_t)blockIdx.x / gridDim.x);
-    const int last = item_at_cost(L, L.total_cost * (int64_t)(blockIdx.x + 1) / gridDim.x);
-    asm volatile("griddepcontrol.launch_dependents;");
-    if (first >= last) return;
     const int n_local = last - first;
-
-    float* const red = reinterpret_cast<float*>(smem + LY::kRed);  // [2][WC][16][RC]
-    const int64_t xs_slot = (L.xs_bytes + 127) / 128 * 128;
-    uint8_t* const xs = smem + LY::kXs;                              // [2][xs_slot]
-    const uint32_t bar = smem_addr(smem + LY::bars(L.xs_bytes));
-    // bar + 0 / 8: table_ready[slot] (count = service warps)
-    // bar + 16 / 24: item_done[slot] (count = compute warps)
-    if (tid == 0) {
-        mbar_init(bar + 0, G::kServiceWarps);
-        mbar_init(bar + 8, G::kServiceWarps);
-        mbar_init(bar + 16, WC);
-        mbar_init(bar + 24, WC);
-    }
-    __syncthreads();
-
-    if (warp >= WC) {
+    {
         // =============================== service warps =========================
-        const int nst = G::kServiceWarps * 32, st = tid - WC * 32;
+        const int nst = NSW * 32;
+        const int lane = st & 31;
         // centroid rows of the next block, prefetched into registers
         constexpr int kItems = TG::kPair ? (kRowsPerCta << K) : (kRowsPerCta * (1 << K) / 8);
-        constexpr int kPer = (kItems + G::kServiceWarps * 32 - 1) / (G::kServiceWarps * 32);
+        constexpr int kPer = (kItems + NSW * 32 - 1) / (NSW * 32);
         constexpr int kRowVecs = TG::kPair ? ((1 << K) + 7) / 8 : 1;
         uint4 src[kPer][kRowVecs];
         auto load_lut = [&](int item, int pi) {
@@ -341,7 +323,7 @@ __global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
             return (i & 1) ? (w >> 16) : (w & 0xFFFFu);
         };
         auto build = [&](int slot) {
-            uint8_t* const tbase = smem + slot * G::kSlotStride;
+            uint8_t* const tbase = smem + slot * slot_stride;
 #pragma unroll
             for (int i = 0; i < kPer; ++i) {
                 const int it = st + i * nst;
@@ -377,6 +359,30 @@ __global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
         };
         auto stage_x = [&](int pi, int xb) {
             const GemvProblem& P = L.prob[pi];
+            if constexpr (XUB > 0) {
+                // v6 layout: [unit u][m][p][wi][q] 16-byte chunks, m stride XMSTR
+                // (= 64 mod 128: batch rows of one chunk group hit disjoint banks)
+                constexpr int WPU = XUB / 4, UPT = 128 / (4 * XUB), XMSTR = 4 * WPU * 64 + 64;
+                const int per_u = L.m_x * 4 * WPU * 4;  // chunks per unit
+                const int chunks = P.n_tiles * UPT * per_u;
+                for (int c = st; c < chunks; c += nst) {
+                    const int u = c / per_u, r = c - u * per_u;
+                    const int m = r / (4 * WPU * 4), r2 = r - m * (4 * WPU * 4);
+                    const int pw = r2 >> 2, qq = r2 & 3;  // pw = p*WPU + wi
+                    const int pp = pw / WPU, wi = pw - pp * WPU;
+                    const int tile = u / UPT, sl = u - tile * UPT;
+                    const int t = sl * XUB + qq * WPU + wi;
+                    const int64_t col = (int64_t)tile * kTileWeights + 256 * pp + 8 * t;
+                    const int64_t nb = (P.cols - col) * 2;
+                    const uint16_t* srow = P.x + (int64_t)m * P.ldx;
+                    uint8_t* dst = xs + xb * xs_slot + ((int64_t)u * L.m_x + m) * XMSTR + r2 * 16;
+                    cp_async16(dst, nb > 0 ? (const void*)(srow + col) : (const void*)srow,
+                               nb >= 16 ? 16 : (nb > 0 ? (int)nb : 0));
+                }
+                cp_async_commit();
+                cp_async_wait_all();
+                return;
+            }
             const int64_t padded = (int64_t)P.n_tiles * kTileWeights;
             const int chunks = (int)(padded / 8);
             for (int m = 0; m < L.m_x; ++m) {
@@ -421,18 +427,41 @@ __global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
             }
         };
 
+        // L2 prefetch (bulk, one instruction per plane) of the top-KPF planes of
+        // an upcoming item, so the compute warps' plane loads hit L2
+        auto prefetch_item = [&](int item) {
+            if constexpr (KPF > 0) {
+                if (st != 0 || item >= last) return;
+                const GemvProblem& P = L.prob[problem_of(L, item)];
+                const int64_t r0 = (int64_t)(item - P.item_begin) * kRowsPerCta;
+                const int64_t nr = P.rows - r0 < kRowsPerCta ? P.rows - r0 : kRowsPerCta;
+                const uint8_t* a = P.planes + r0 * P.row_bytes;
+                const uint32_t bytes = (uint32_t)(nr * P.row_bytes);
+#pragma unroll 1
+                for (int pl = 0; pl < KPF; ++pl)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + (int64_t)pl * P.plane_stride),
+                                 "r"(bytes)
+                                 : "memory");
+            }
+        };
+        prefetch_item(first + 1);
+        prefetch_item(first + 2);
         // activations / outputs may belong to the previous kernel in the stream
         asm volatile("griddepcontrol.wait;" ::: "memory");
         int pi = problem_of(L, first), pend = problem_end(L, pi);
-        int xb = 0, pi_hist[2] = {pi, pi};
+        int xb = 0, pi_hist[NSLOT];
+#pragma unroll
+        for (int i = 0; i < NSLOT; ++i) pi_hist[i] = pi;
         load_lut(first, pi);
 #pragma unroll 1
-        for (int jl = 0; jl < n_local + 2; ++jl) {
-            if (jl >= 2) {  // block jl-2 finished by every compute warp: reduce it, free its slot
-                mbar_wait(bar + 16 + 8 * (jl & 1), ((jl - 2) >> 1) & 1);
-                reduce(first + jl - 2, pi_hist[jl & 1], jl & 1);
+        for (int jl = 0; jl < n_local + NSLOT; ++jl) {
+            const int sl = jl % NSLOT;
+            if (jl >= NSLOT) {  // item jl-NSLOT finished by every compute warp: reduce it, free its slot
+                mbar_wait(bar + 8 * NSLOT + 8 * sl, ((jl - NSLOT) / NSLOT) & 1);
+                reduce(first + jl - NSLOT, pi_hist[sl], sl);
             }
             if (jl < n_local) {
+                prefetch_item(first + jl + 3);
                 const int item = first + jl;
                 if (item >= pend) {  // next layer of a grouped launch
                     pi = problem_of(L, item);
@@ -442,17 +471,61 @@ __global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
                 } else if (jl == 0) {
                     if constexpr (XS) stage_x(pi, xb);
                 }
-                pi_hist[jl & 1] = pi;
-                build(jl & 1);
+                pi_hist[sl] = pi;
+                build(sl);
                 // prefetch the next block's centroid rows while this one is consumed
                 if (item + 1 < last) {
                     const int npi = item + 1 >= pend ? problem_of(L, item + 1) : pi;
                     load_lut(item + 1, npi);
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar + 8 * (jl & 1));
+                if (lane == 0) mbar_arrive(bar + 8 * sl);
             }
         }
+    }
+}
+
+template <int K, int NG, int UB, bool XS>
+__global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
+    gemv_kernel(const __grid_constant__ GemvLaunch L) {
+    using V = UnitVec<UB>;
+    using VT = typename V::T;
+    using TG = TableGeom<K>;
+    using G = WsGeom<K, NG>;
+    using LY = WsLayout<K, NG>;
+    constexpr int WC = G::kComputeWarps;
+    constexpr int WPU = UB / 4;          // lane words per unit per row
+    constexpr int UPT = 128 / (4 * UB);  // units per tile
+    constexpr int RC = 8 * NG;           // reduction columns
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, q = lane & 3;
+    if (smem_addr(smem) != APB_SMEM_BASE) __trap();  // see lds_table
+
+    const int first = item_at_cost(L, L.total_cost * (int64_t)blockIdx.x / gridDim.x);
+    const int last = item_at_cost(L, L.total_cost * (int64_t)(blockIdx.x + 1) / gridDim.x);
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (first >= last) return;
+    const int n_local = last - first;
+
+    float* const red = reinterpret_cast<float*>(smem + LY::kRed);  // [2][WC][16][RC]
+    const int64_t xs_slot = (L.xs_bytes + 127) / 128 * 128;
+    uint8_t* const xs = smem + LY::kXs;                              // [2][xs_slot]
+    const uint32_t bar = smem_addr(smem + LY::bars(L.xs_bytes));
+    // bar + 0 / 8: table_ready[slot] (count = service warps)
+    // bar + 16 / 24: item_done[slot] (count = compute warps)
+    if (tid == 0) {
+        mbar_init(bar + 0, G::kServiceWarps);
+        mbar_init(bar + 8, G::kServiceWarps);
+        mbar_init(bar + 16, WC);
+        mbar_init(bar + 24, WC);
+    }
+    __syncthreads();
+
+    if (warp >= WC) {
+        service_role<K, G::kServiceWarps, WC, RC, XS>(L, first, last, smem, bar, red, xs, xs_slot,
+                                                      tid - WC * 32, G::kSlotStride);
         return;
     }
 
@@ -648,6 +721,218 @@ __global__ void __launch_bounds__(WsGeom<K, NG>::kThreads, 1)
 #endif
 }
 
+// ---- v6: lean batch <= 8 kernel ---------------------------------------------
+// Same roles, tables, hand-offs and arithmetic (bit-identical results) as the
+// v5 kernel above, with a compute loop stripped to the essential instruction
+// stream per lane word: k plane words -> bit network -> PRMT + LDS per lookup
+// -> HMMA.  Differences: activations always come from shared memory and every
+// lane loads its B fragment (columns n >= m_x are never read back, so no
+// zeroing); rows past the layer end are clamped onto its last row instead of
+// predicated (their outputs are never stored); the plane walker keeps one
+// 64-bit pointer plus 32-bit offsets.
+template <int K, int UB>
+struct G6 {
+    static constexpr int kTotalWarps = K >= 7 ? 12 : 16;
+    static constexpr int kServiceWarps = 2;
+    static constexpr int kWC = kTotalWarps - kServiceWarps;
+    static constexpr int kThreads = kTotalWarps * 32;
+    static constexpr int kUPT = 128 / (4 * UB);  // units per tile
+    static constexpr int kLgUPT = kUPT == 2 ? 1 : (kUPT == 4 ? 2 : 3);
+    static constexpr int kWPU = UB / 4;          // lane words per unit per row
+    static constexpr int kSlotStride = 64 * 1024;
+    // table slots: 3 where they fit next to the rest (more slack between a
+    // table's build and its first use), else 2
+#ifndef APB_SLOTS3_MAXB
+#define APB_SLOTS3_MAXB (32 * 1024)
+#endif
+    static constexpr int kSlots = TableGeom<K>::kBytes <= APB_SLOTS3_MAXB ? 3 : 2;
+    static constexpr int kRedBytes = kWC * kRowsPerCta * 8 * 4;  // one slot
+    static constexpr int kRed = (kSlots - 1) * kSlotStride + TableGeom<K>::kBytes;
+    static constexpr int kXs = kRed + kSlots * kRedBytes;
+    static constexpr int kXmStride = 4 * kWPU * 64 + 64;  // x bytes per (unit, batch row)
+    __host__ __device__ static int64_t xs_bytes(int64_t padded, int m_x) {
+        return padded / (4 * UB * 8) * m_x * kXmStride;
+    }
+    __host__ __device__ static size_t bars(int64_t xs_bytes) { return (size_t)kXs + 2 * (size_t)((xs_bytes + 127) / 128 * 128); }
+    __host__ __device__ static size_t total(int64_t xs_bytes) { return bars(xs_bytes) + 16 * kSlots; }
+};
+
+template <int K, int UB>
+__global__ void __launch_bounds__(G6<K, UB>::kThreads, 1) gemv6_kernel(const __grid_constant__ GemvLaunch L) {
+    using V = UnitVec<UB>;
+    using VT = typename V::T;
+    using G = G6<K, UB>;
+    constexpr int WC = G::kWC, UPT = G::kUPT, LG = G::kLgUPT, WPU = G::kWPU;
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, q = lane & 3;
+    if (smem_addr(smem) != APB_SMEM_BASE) __trap();  // see lds_table
+
+    const int first = item_at_cost(L, L.total_cost * (int64_t)blockIdx.x / gridDim.x);
+    const int last = item_at_cost(L, L.total_cost * (int64_t)(blockIdx.x + 1) / gridDim.x);
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (first >= last) return;
+    const int n_local = last - first;
+
+    float* const red = reinterpret_cast<float*>(smem + G::kRed);  // [2][WC][16][8]
+    const int64_t xs_slot = (L.xs_bytes + 127) / 128 * 128;
+    uint8_t* const xs = smem + G::kXs;
+    const uint32_t bar = smem_addr(smem + G::bars(L.xs_bytes));
+    constexpr int NS = G::kSlots;
+    // bar + 8s: table_ready[s] (count = service warps); bar + 8(NS + s): item_done[s]
+    if (tid == 0) {
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(bar + 8 * i, G::kServiceWarps);
+            mbar_init(bar + 8 * (NS + i), WC);
+        }
+    }
+    __syncthreads();
+
+    if (warp >= WC) {
+#ifndef APB_PF
+#define APB_PF 1
+#endif
+        service_role<K, G::kServiceWarps, WC, 8, true, UB, NS, APB_PF ? K : 0>(L, first, last, smem, bar, red, xs, xs_slot,
+                                                                  tid - WC * 32, G::kSlotStride);
+        return;
+    }
+
+    // ---- plane walker: next unit (item lj, unit lv) this warp loads ----
+    int lj = 0, lv = warp, lpi = problem_of(L, first), lpend = problem_end(L, lpi), lU = 0;
+    uint32_t lps = 0;
+    int32_t ld1 = 0;
+    const uint8_t* lb0 = nullptr;
+    auto lset = [&](int item) {
+        const GemvProblem& P = L.prob[lpi];
+        lU = P.n_tiles * UPT;
+        lps = (uint32_t)P.plane_stride;
+        const int64_t r0 = (int64_t)(item - P.item_begin) * kRowsPerCta + g;
+        const int64_t ra = r0 < P.rows ? r0 : P.rows - 1;
+        const int64_t rb = r0 + 8 < P.rows ? r0 + 8 : P.rows - 1;
+        lb0 = P.planes + ra * P.row_bytes + q * UB;
+        ld1 = (int32_t)((rb - ra) * P.row_bytes);
+    };
+    lset(first);
+    bool ldone = false;
+    auto lnorm = [&]() {
+#pragma unroll 1
+        while (lv >= lU) {
+            lv -= lU;
+            if (++lj >= n_local) {
+                ldone = true;
+                return;
+            }
+            const int item = first + lj;
+            if (item >= lpend) {
+                ++lpi;
+#pragma unroll 1
+                while (item >= problem_end(L, lpi)) ++lpi;
+                lpend = problem_end(L, lpi);
+            }
+            lset(item);
+        }
+    };
+    lnorm();
+    auto lload = [&](VT(&dst)[2][K]) {
+        if (ldone) return;
+        const uint8_t* p0 = lb0 + (((uint32_t)lv >> LG) * (uint32_t)kTileBytes + ((uint32_t)lv & (UPT - 1)) * (4u * UB));
+        const uint8_t* p1 = p0 + ld1;
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+            dst[0][K - 1 - p] = V::load(p0);
+            dst[1][K - 1 - p] = V::load(p1);
+            p0 += lps;
+            p1 += lps;
+        }
+        lv += WC;
+        lnorm();
+    };
+
+    VT bufA[2][K], bufB[2][K];
+    lload(bufA);
+    lload(bufB);
+
+    // B fragment: only lanes whose batch column n = g is real load x; the
+    // others keep don't-care registers (MMA columns are independent and
+    // columns n >= m_x are never read back)
+    const uint32_t xlive = g < L.m_x ? 1u : 0u;
+    int cpi = problem_of(L, first), cpend = problem_end(L, cpi), xb = 0;
+    int U = L.prob[cpi].n_tiles * UPT;
+    int gu = warp, ring = 0;
+#pragma unroll 1
+    for (int jl = 0; jl < n_local; ++jl) {
+        const int item = first + jl;
+        if (item >= cpend) {
+            cpi = problem_of(L, item);
+            cpend = problem_end(L, cpi);
+            xb ^= 1;
+            U = L.prob[cpi].n_tiles * UPT;
+        }
+        const uint32_t xrow = smem_addr(xs + xb * xs_slot) + (uint32_t)g * G::kXmStride + (uint32_t)q * 16u;
+        const uint32_t xustride = (uint32_t)L.m_x * G::kXmStride;
+        const int sl = jl % NS;
+        const uint32_t off0 = ((uint32_t)sl << 16) | ((uint32_t)lane * 4u), off1 = off0 + 128u;
+        float acc[2][4];
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) acc[c2][0] = acc[c2][1] = acc[c2][2] = acc[c2][3] = 0.f;
+
+        auto unit = [&](int u, const VT(&buf)[2][K]) {
+            // lane word t = s*UB + q*WPU + wi of tile `tile`; x columns 256p + 8t + 0..7
+            const uint32_t xa = xrow + (uint32_t)u * xustride;
+#pragma unroll
+            for (int wi = 0; wi < WPU; ++wi) {
+                uint4 xv[4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    xv[p] = make_uint4(0, 0, 0, 0);
+                    lds128_pred(xv[p], xa + (p * WPU + wi) * 64, xlive);
+                }
+                uint32_t Q0[K], Q1[K];
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                    Q0[i] = V::word(buf[0][i], wi);
+                    Q1[i] = V::word(buf[1][i], wi);
+                }
+                uint32_t a0[16], a1[16];
+                decode_word<K>(Q0, off0, a0);
+                decode_word<K>(Q1, off1, a1);
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj)
+                        mma16816(acc[p & 1], a0[p * 4 + 2 * jj], a1[p * 4 + 2 * jj], a0[p * 4 + 2 * jj + 1],
+                                 a1[p * 4 + 2 * jj + 1], u4_word(xv[p], 2 * jj), u4_word(xv[p], 2 * jj + 1));
+            }
+        };
+
+        mbar_wait(bar + 8 * sl, (jl / NS) & 1);  // this item's table (and x) ready
+#pragma unroll 1
+        for (; gu < U; gu += WC) {
+            if (ring) {
+                unit(gu, bufB);
+                lload(bufB);
+            } else {
+                unit(gu, bufA);
+                lload(bufA);
+            }
+            ring ^= 1;
+        }
+        gu -= U;
+        float* r = red + sl * (WC * kRowsPerCta * 8) + (warp * kRowsPerCta + g) * 8 + 2 * q;
+        r[0] = acc[0][0] + acc[1][0];
+        r[1] = acc[0][1] + acc[1][1];
+        r[8 * 8] = acc[0][2] + acc[1][2];
+        r[8 * 8 + 1] = acc[0][3] + acc[1][3];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar + 8 * (NS + sl));
+    }
+}
+
+template <int K, int UB>
+static int launch6(const GemvLaunch& L, cudaStream_t s);
+
 constexpr int64_t kMaxXsBytes = 48 * 1024;
 constexpr size_t kSmemLimitBytes = 227 * 1024;
 
@@ -700,9 +985,53 @@ constexpr int unit_bytes() {
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
+template <int K, int UB>
+static int launch6(const GemvLaunch& L, cudaStream_t s) {
+    using G = G6<K, UB>;
+    auto kern = gemv6_kernel<K, UB>;
+    static std::atomic<int> configured{0};
+    if (!configured.load(std::memory_order_acquire)) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimitBytes) != cudaSuccess)
+            return APB_ERR_CUDA;
+        configured.store(1, std::memory_order_release);
+    }
+    const size_t smem = G::total(L.xs_bytes);
+    int grid = sm_count();
+    if (grid > L.n_items) grid = L.n_items;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)G::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (L.flags & APB_FLAG_PDL) ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, kern, L) != cudaSuccess) return APB_ERR_CUDA;
+    return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
+}
+
+static bool use_v6() {
+    static const int v = [] {
+        const char* e = std::getenv("APB_GEMV_V5");
+        return (e && e[0] == '1') ? 0 : 1;
+    }();
+    return v != 0;
+}
+
 template <int K, int NG>
 static int dispatch_xs(GemvLaunch& L, cudaStream_t s) {
     if constexpr (NG == 1) {
+        if (use_v6() && L.m_x <= 8) {
+            using G = G6<K, unit_bytes<K>()>;
+            GemvLaunch L6 = L;
+            int64_t mp = 0;
+            for (int i = 0; i < L.n_prob; ++i)
+                mp = L.prob[i].n_tiles > mp ? L.prob[i].n_tiles : mp;
+            L6.xs_bytes = G::xs_bytes(mp * kTileWeights, L.m_x);
+            if (G::total(L6.xs_bytes) <= kSmemLimit) return launch6<K, unit_bytes<K>()>(L6, s);
+        }
         // activations in shared memory when both buffers fit next to the tables
         if (L.xs_bytes > 0 && L.xs_bytes <= kMaxXsBytes && WsLayout<K, NG>::total(L.xs_bytes) <= kSmemLimit)
             return launch_variant<K, NG, unit_bytes<K>(), true>(L, s);
@@ -775,6 +1104,11 @@ static int gemv_launch_chunk(int n, const uint8_t* const* planes, const int64_t*
     return APB_ERR_PARAM;
 }
 
+extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
+                             const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
+                             const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split,
+                             void* const* y, int y_dtype, const int64_t* ldy, int64_t y_off, int flags, void* stream);
+
 extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, const int* n_max,
                                 const int64_t* rows, const int64_t* cols,
                                 const int64_t* padded_cols, int k, const uint16_t* const* lut,
@@ -796,6 +1130,11 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
         if (ldy[i] < rows[i]) return APB_ERR_SHAPE;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    if (m_x <= 2 && n_problems <= 16) {  // TMA-fed kernel (apb_gemv7.cu)
+        const int rc = apb7_try_gemv(n_problems, planes, n_max, rows, cols, padded_cols, k, lut, x, m_x, ldx, 0,
+                                     x_split, y, y_dtype, ldy, 0, flags, stream);
+        if (rc != -1) return rc;
+    }
     // batch columns per launch: 32 fp16 activation rows (4 mma column groups)
     const int chunk = 32;
     for (int p0 = 0; p0 < n_problems; p0 += kMaxGroup) {

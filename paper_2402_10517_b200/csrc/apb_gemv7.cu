@@ -1,0 +1,627 @@
+// apb_gemv7.cu -- TMA-fed bitplane GEMV for batch <= 2 (sm_100a).
+//
+// Replaces engine.py:284-309 (gemv) and the M <= 2 case of engine.py:312-341
+// (gemm, quantized path) of the reference: y[m][r] = sum_c LUT_k[r][code_k(r,c)]
+// * x[m][c], reading ONLY planes 0..k-1 and the k-bit centroid table.
+//
+// Why a second kernel: the register-streaming kernels (apb_gemv.cu) load the
+// planes with warp-wide LDGs that touch 8 rows x 32 B each, which keeps the
+// L1 tag stage ~70 % busy at ~40 % of HBM bandwidth.  Here the planes never
+// pass through the LSU: a producer thread streams them with TMA
+// (cp.async.bulk.tensor, 3-D map {row bytes, rows, planes}, 128-B swizzle)
+// into a ring of shared-memory stages, one stage = one 1024-column tile x 16
+// rows x k planes, and the compute warps read them back with conflict-free
+// LDS.128.  The centroid rows of each item are brought in the same way.
+//
+// Lane mapping ("row copies"): lane (g, q) of a compute warp owns row
+// 2g + (q >> 1) of the 16-row item, copy q & 1.  Rows 2g / 2g+1 share one MMA
+// row (g for columns set A, g + 8 for set B); the B operand is block-sparse:
+// column 0 holds x on the k-slots of lanes q = 0,1 (row 2g, set A), column 1
+// on those of q = 2,3 (row 2g+1), columns 2/3 likewise for set B, columns 4..7
+// the same for the second batch row.  So every lane looks up ITS row only and
+// a table needs 2 copies per row (one per lane) instead of 4 -- half the
+// table bytes and build work of the 16-row mapping, with every lookup still
+// bank-conflict free (bank = lane).
+//
+// Numerics are those of the other kernels: fp16 table entries, fp16
+// activations, fp32 MMA accumulation, a fixed reduction order (per-warp
+// partials summed in warp order) -> bit-reproducible.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/anyprec_b200.h"
+#include "apb_common.cuh"
+
+namespace apb7 {
+using apb::kTileBytes;
+using apb::kTileWeights;
+using apb::prmt;
+
+constexpr int kRows = 16;      // rows per item
+constexpr int kMaxProb = 16;   // problems per grouped launch
+constexpr int kSmemBase = 1024;  // sm_100 reserves the first 1 KB of the shared window
+
+struct Prob7 {
+    const uint16_t* x;  // fp16 [m_x][ldx]
+    void* y;            // [m_out][ldy]
+    int64_t rows, cols, ldx, ldy;
+    int n_tiles;
+    int item_begin;
+    int64_t cost_begin;
+};
+
+struct alignas(64) Launch7 {
+    CUtensorMap tm_planes[kMaxProb];  // 3-D {row_bytes, rows, n_max} u8, box {128, 16, 1}, 128B swizzle
+    CUtensorMap tm_lut[kMaxProb];     // 2-D {2^k, rows} f16, box {min(2^k, 64), 16}
+    Prob7 prob[kMaxProb];
+    int n_prob, n_items;
+    int64_t total_cost;
+    int m_x, x_split, y_f16;
+    int n_stages;      // ring depth
+    int64_t xs_bytes;  // one activation buffer
+};
+
+template <int K>
+struct Geo {
+    static constexpr bool kPair = K <= 4;
+    static constexpr int kEntries = kPair ? (1 << (2 * K)) : (1 << K);
+    static constexpr int kTableBytes = kEntries * 256;  // [entry][slot 2][lane 32] u32
+    static constexpr int kLutHalves = 1 << K;
+    static constexpr int kLutBox = kLutHalves < 64 ? kLutHalves : 64;  // halves per box row
+    static constexpr int kLutBoxes = kLutHalves / kLutBox;
+    static constexpr int kLutBytes = kRows * kLutHalves * 2;
+    static constexpr int kLutSlot = (kLutBytes + 1023) / 1024 * 1024;
+    static constexpr int kStageBytes = K * 2048;  // 16 rows x 128 B x K planes
+    static constexpr int kWC = 12;                // compute warps: 3 groups of 4
+    static constexpr int kNG = kWC / 4;
+    static constexpr int kThreads = (kWC + 2) * 32;
+    static constexpr int kRedBytes = 2 * kWC * 2 * kRows * 4;  // [slot][warp][m][row] f32
+    // layout: tables | lut x2 | ring | xs x2 | red | barriers
+    static constexpr int kLut = (kTableBytes + 1023) / 1024 * 1024;
+    static constexpr int kRing = kLut + 2 * kLutSlot;
+    static size_t total(int n_stages, int64_t xs_bytes) {
+        return (size_t)kRing + (size_t)n_stages * kStageBytes + 2 * (size_t)xs_bytes + kRedBytes + 256;
+    }
+};
+
+// ---- PTX helpers ---------------------------------------------------------------
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("{\n\t.reg .b64 s;\n\tmbarrier.arrive.shared::cta.b64 s, [%0];\n\t}" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 s;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 s, [%0], %1;\n\t}" ::"r"(a),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma2(uint32_t dst, const CUtensorMap* m, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(m), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+// B-fragment load: executed only where pred != 0; other lanes keep their
+// (zero) registers -- the B operand is block-sparse by construction.
+__device__ __forceinline__ void lds128_keep(uint32_t& v0, uint32_t& v1, uint32_t& v2, uint32_t& v3, uint32_t a,
+                                            uint32_t pred) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t"
+        "@p ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
+        : "+r"(v0), "+r"(v1), "+r"(v2), "+r"(v3)
+        : "r"(a), "r"(pred));
+}
+__device__ __forceinline__ uint32_t u4w(const uint4& v, int i) {
+    return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+__device__ __forceinline__ uint32_t lds_table(uint32_t off) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+1024];" : "=r"(v) : "r"(off));
+    return v;
+}
+__device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(src_bytes));
+}
+
+__device__ __forceinline__ int problem_of(const Launch7& L, int item) {
+    int pi = 0;
+#pragma unroll 1
+    for (int i = 1; i < L.n_prob; ++i)
+        if (item >= L.prob[i].item_begin) pi = i;
+    return pi;
+}
+__device__ __forceinline__ int problem_end(const Launch7& L, int pi) {
+    return pi + 1 < L.n_prob ? L.prob[pi + 1].item_begin : L.n_items;
+}
+__device__ __forceinline__ int item_at_cost(const Launch7& L, int64_t target) {
+    if (target >= L.total_cost) return L.n_items;
+#pragma unroll 1
+    for (int i = 0; i < L.n_prob; ++i) {
+        const Prob7& P = L.prob[i];
+        const int n = problem_end(L, i) - P.item_begin;
+        const int64_t end = P.cost_begin + (int64_t)n * P.n_tiles;
+        if (target < end) return P.item_begin + (int)((target - P.cost_begin + P.n_tiles - 1) / P.n_tiles);
+    }
+    return L.n_items;
+}
+
+// Decode one lane word into 16 fp16x2 A values: out[p*4 + j] = weights of
+// columns (256p + 8t + 2j, +1) of this lane's row (apb_common.cuh networks).
+template <int K>
+__device__ __forceinline__ void decode_word(const uint32_t* Q, uint32_t off, uint32_t* out) {
+    if constexpr (Geo<K>::kPair) {
+        uint32_t U[4];
+        apb::to_pairs<K>(Q, U);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) out[p * 4 + j] = lds_table(prmt(U[j], off, 0x7604u | (uint32_t)(p << 4)));
+    } else {
+        uint32_t Wb[8];
+        apb::to_bytes<K>(Q, Wb);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const uint32_t sel = 0x7604u | (uint32_t)(p << 4);
+                const uint32_t e = lds_table(prmt(Wb[2 * j], off, sel));
+                const uint32_t o = lds_table(prmt(Wb[2 * j + 1], off, sel));
+                out[p * 4 + j] = e + (o << 16);  // entries are (v, 0): one IMAD packs the pair
+            }
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid_constant__ Launch7 L) {
+    using G = Geo<K>;
+    constexpr int WC = G::kWC, NG = G::kNG;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (saddr(smem) != kSmemBase) __trap();  // lds_table folds the table base into the immediate
+
+    const int first = item_at_cost(L, L.total_cost * (int64_t)blockIdx.x / gridDim.x);
+    const int last = item_at_cost(L, L.total_cost * (int64_t)(blockIdx.x + 1) / gridDim.x);
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (first >= last) return;
+    const int n_local = last - first;
+    const int NST = L.n_stages;
+
+    const uint32_t s_lut = saddr(smem + G::kLut);
+    const uint32_t s_ring = saddr(smem + G::kRing);
+    uint8_t* const xs = smem + G::kRing + (size_t)NST * G::kStageBytes;
+    float* const red = reinterpret_cast<float*>(xs + 2 * L.xs_bytes);
+    const uint32_t bar = saddr(reinterpret_cast<uint8_t*>(red) + G::kRedBytes);
+    // barriers (8 B each): full[NST] | empty[NST] | lut_full[2] | lut_empty[2] | table_ready[2] | item_done[2]
+    const uint32_t b_full = bar, b_empty = bar + 8 * NST, b_lfull = bar + 16 * NST, b_lempty = b_lfull + 16,
+                   b_tready = b_lfull + 32, b_idone = b_lfull + 48;
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(b_full + 8 * i, 1);
+            mbar_init(b_empty + 8 * i, 4);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(b_lfull + 8 * i, 1);
+            mbar_init(b_lempty + 8 * i, 1);
+            mbar_init(b_tready + 8 * i, 1);
+            mbar_init(b_idone + 8 * i, WC);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == WC) {
+        // ============================ producer (TMA) ============================
+        if (lane != 0) return;
+        int gs = 0;
+        int pi = problem_of(L, first), pend = problem_end(L, pi);
+#pragma unroll 1
+        for (int jl = 0; jl < n_local; ++jl) {
+            const int item = first + jl;
+            if (item >= pend) {
+                pi = problem_of(L, item);
+                pend = problem_end(L, pi);
+            }
+            const Prob7& P = L.prob[pi];
+            const int row0 = (item - P.item_begin) * kRows;
+            // centroid rows of the item -> lut slot jl & 1
+            if (jl >= 2) mbar_wait(b_lempty + 8 * (jl & 1), ((jl - 2) >> 1) & 1);
+            mbar_expect_tx(b_lfull + 8 * (jl & 1), G::kLutBytes);
+#pragma unroll
+            for (int b = 0; b < G::kLutBoxes; ++b)
+                tma2(s_lut + (jl & 1) * G::kLutSlot + b * (kRows * G::kLutBox * 2), &L.tm_lut[pi], b * G::kLutBox, row0,
+                     b_lfull + 8 * (jl & 1));
+            // plane tiles -> ring stages
+#pragma unroll 1
+            for (int t = 0; t < P.n_tiles; ++t, ++gs) {
+                const int slot = gs % NST, ph = gs / NST;
+                if (ph > 0) mbar_wait(b_empty + 8 * slot, (ph - 1) & 1);
+                mbar_expect_tx(b_full + 8 * slot, G::kStageBytes);
+                const uint32_t dst = s_ring + slot * G::kStageBytes;
+#pragma unroll
+                for (int p = 0; p < K; ++p) tma3(dst + p * 2048, &L.tm_planes[pi], t * kTileBytes, row0, p, b_full + 8 * slot);
+            }
+        }
+        return;
+    }
+
+    if (warp == WC + 1) {
+        // ========================= service: tables, x, y =========================
+        const int g = lane >> 2, q = lane & 3, rho = 2 * g + (q >> 1);
+        auto stage_x = [&](int pi, int xb) {
+            // [m][tile][t 32][half 2][p 4][4 halves]: 8-byte chunks, zero past cols
+            const Prob7& P = L.prob[pi];
+            const int chunks = L.m_x * P.n_tiles * 256;
+            const uint32_t base = saddr(xs + xb * L.xs_bytes);
+            for (int c = lane; c < chunks; c += 32) {
+                const int m = c / (P.n_tiles * 256), r = c - m * (P.n_tiles * 256);
+                const int tile = r >> 8, w = r & 255;
+                const int t = w >> 3, half = (w >> 2) & 1, p = w & 3;
+                const int64_t col = (int64_t)tile * kTileWeights + 256 * p + 8 * t + 4 * half;
+                const int64_t nb = (P.cols - col) * 2;
+                const uint16_t* src = P.x + (int64_t)m * P.ldx;
+                cp_async8(base + (uint32_t)(m * P.n_tiles * 2048 + r * 8), nb > 0 ? (const void*)(src + col) : (const void*)src,
+                          nb >= 8 ? 8 : (nb > 0 ? (int)nb : 0));
+            }
+            asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+        };
+        auto build = [&](int slot) {
+            // this lane's table column: row rho, copy q & 1 -> [entry][slot][lane]
+            const uint32_t lut = s_lut + slot * G::kLutSlot;
+            const uint32_t dst = saddr(smem) + slot * 128 + lane * 4;
+            if constexpr (G::kPair) {
+                uint32_t h[1 << K];
+                if constexpr (K == 3) {
+                    const uint4 v = lds128(lut + rho * 16);
+                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) h[i] = (i & 1) ? (w4[i >> 1] >> 16) : (w4[i >> 1] & 0xFFFFu);
+                } else {  // K == 4: 32-byte rows
+                    const uint4 v0 = lds128(lut + rho * 32), v1 = lds128(lut + rho * 32 + 16);
+                    const uint32_t w8[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) h[i] = (i & 1) ? (w8[i >> 1] >> 16) : (w8[i >> 1] & 0xFFFFu);
+                }
+#pragma unroll
+                for (int idx = 0; idx < G::kEntries; ++idx) {
+                    uint32_t ce, co;
+                    apb::pair_codes<K>((uint32_t)idx, ce, co);
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(dst + idx * 256), "r"(h[ce] | (h[co] << 16)) : "memory");
+                }
+            } else {
+#pragma unroll 4
+                for (int cc = 0; cc < G::kLutHalves / 8; ++cc) {
+                    // 16-byte chunk cc of row rho (box layout + swizzle of the LUT map)
+                    const int b = cc / 8, ci = cc % 8;
+                    uint32_t a;
+                    if constexpr (K == 5) a = rho * 64 + ((ci ^ ((rho >> 1) & 3)) << 4);
+                    else a = b * (kRows * 128) + rho * 128 + ((ci ^ (rho & 7)) << 4);
+                    const uint4 v = lds128(lut + a);
+                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const uint32_t e = (i & 1) ? (w4[i >> 1] >> 16) : (w4[i >> 1] & 0xFFFFu);
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(dst + (cc * 8 + i) * 256), "r"(e) : "memory");
+                    }
+                }
+            }
+        };
+        auto reduce = [&](int item, int pi, int slot) {
+            const Prob7& P = L.prob[pi];
+            const int m_out = L.x_split ? 1 : L.m_x;
+            const int64_t row0 = (int64_t)(item - P.item_begin) * kRows;
+            const float* r = red + slot * (WC * 2 * kRows);
+            for (int i = lane; i < kRows * m_out; i += 32) {
+                const int rl = i & 15, m = i >> 4;
+                const int64_t row = row0 + rl;
+                if (row >= P.rows) continue;
+                float sum;
+                if (L.x_split) {
+                    float hi = 0.f, lo = 0.f;
+#pragma unroll
+                    for (int w = 0; w < WC; ++w) hi += r[(w * 2 + 0) * kRows + rl];
+#pragma unroll
+                    for (int w = 0; w < WC; ++w) lo += r[(w * 2 + 1) * kRows + rl];
+                    sum = hi + lo;
+                } else {
+                    sum = 0.f;
+#pragma unroll
+                    for (int w = 0; w < WC; ++w) sum += r[(w * 2 + m) * kRows + rl];
+                }
+                if (L.y_f16)
+                    reinterpret_cast<__half*>(P.y)[(int64_t)m * P.ldy + row] = __float2half_rn(sum);
+                else
+                    reinterpret_cast<float*>(P.y)[(int64_t)m * P.ldy + row] = sum;
+            }
+        };
+
+        int pi = problem_of(L, first), pend = problem_end(L, pi);
+        int xb = 0, pi_hist[2] = {pi, pi};
+#pragma unroll 1
+        for (int jl = 0; jl < n_local + 2; ++jl) {
+            if (jl >= 2) {  // item jl-2 done by every compute warp: reduce it, free its slot
+                mbar_wait(b_idone + 8 * (jl & 1), ((jl - 2) >> 1) & 1);
+                reduce(first + jl - 2, pi_hist[jl & 1], jl & 1);
+            }
+            if (jl < n_local) {
+                const int item = first + jl;
+                bool new_x = jl == 0;
+                if (item >= pend) {
+                    pi = problem_of(L, item);
+                    pend = problem_end(L, pi);
+                    xb ^= 1;
+                    new_x = true;
+                }
+                pi_hist[jl & 1] = pi;
+                mbar_wait(b_lfull + 8 * (jl & 1), (jl >> 1) & 1);
+                build(jl & 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(b_lempty + 8 * (jl & 1));
+                if (jl == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // x / y of earlier kernels
+                if (new_x) stage_x(pi, xb);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(b_tready + 8 * (jl & 1));
+            }
+        }
+        return;
+    }
+
+    // =============================== compute warps ===============================
+    const int g = lane >> 2, q = lane & 3;
+    const int rho = 2 * g + (q >> 1), cp = q & 1;
+    const int grp = warp >> 2, su = warp & 3;
+    const int ch = su + 4 * cp;  // 16-byte chunk of the tile row: words 4ch .. 4ch+3
+    const uint32_t plane_off = rho * 128 + ((ch ^ (rho & 7)) << 4);  // 128B-swizzled stage row
+    // B fragment role: column n = g; batch row m = g >> 2, set = (g >> 1) & 1
+    const int gm = g >> 2, gset = (g >> 1) & 1;
+    const uint32_t xlive = (gm < L.m_x && (q >> 1) == (g & 1)) ? 1u : 0u;
+    const uint32_t x_lane = (uint32_t)(4 * ch) * 64u + (uint32_t)gset * 32u;  // + tile*2048 + wi*64 + {0,16}
+
+    uint32_t xr[2][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) xr[0][i] = xr[1][i] = 0u;
+
+    int pi = problem_of(L, first), pend = problem_end(L, pi), xb = 0;
+    int gs = grp;           // next ring stage of this warp group
+    int item_gs = 0;        // first stage of the current item
+#pragma unroll 1
+    for (int jl = 0; jl < n_local; ++jl) {
+        const int item = first + jl;
+        if (item >= pend) {
+            pi = problem_of(L, item);
+            pend = problem_end(L, pi);
+            xb ^= 1;
+        }
+        const int nt = L.prob[pi].n_tiles;
+        const uint32_t xrow = saddr(xs + xb * L.xs_bytes) + (uint32_t)gm * (uint32_t)(nt * 2048) + x_lane;
+        const uint32_t off = (uint32_t)(jl & 1) * 128u + (uint32_t)lane * 4u;
+        float acc[2][4];
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) acc[c2][0] = acc[c2][1] = acc[c2][2] = acc[c2][3] = 0.f;
+
+        mbar_wait(b_tready + 8 * (jl & 1), (jl >> 1) & 1);  // table (and x) of this item
+#pragma unroll 1
+        for (; gs < item_gs + nt; gs += NG) {
+            const int tile = gs - item_gs;
+            const int slot = gs % NST, ph = gs / NST;
+            mbar_wait(b_full + 8 * slot, ph & 1);
+            const uint32_t sb = s_ring + slot * G::kStageBytes + plane_off;
+            uint4 pv[K];
+#pragma unroll
+            for (int p = 0; p < K; ++p) pv[K - 1 - p] = lds128(sb + p * 2048);  // Q[i] = plane K-1-i (LSB first)
+            const uint32_t xa = xrow + (uint32_t)tile * 2048u;
+#pragma unroll
+            for (int wi = 0; wi < 4; ++wi) {
+                uint32_t(&xv)[8] = xr[wi & 1];
+                lds128_keep(xv[0], xv[1], xv[2], xv[3], xa + wi * 64, xlive);
+                lds128_keep(xv[4], xv[5], xv[6], xv[7], xa + wi * 64 + 16, xlive);
+                uint32_t Q[K];
+#pragma unroll
+                for (int i = 0; i < K; ++i) Q[i] = u4w(pv[i], wi);
+                uint32_t a[16];
+                decode_word<K>(Q, off, a);
+                if (wi == 0) {  // every plane register has been consumed: release the stage
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(b_empty + 8 * slot);
+                }
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+                    mma16816(acc[p & 1], a[p * 4 + 0], a[p * 4 + 2], a[p * 4 + 1], a[p * 4 + 3], xv[2 * p], xv[2 * p + 1]);
+            }
+        }
+        item_gs += nt;
+        // rows 2g / 2g+1 of batch row q>>1: D[g][2q'] + D[g+8][2q'+2] with q' = q & 2
+        float c[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c[i] = acc[0][i] + acc[1][i];
+        const float o2 = __shfl_xor_sync(0xffffffffu, c[2], 1), o3 = __shfl_xor_sync(0xffffffffu, c[3], 1);
+        if ((q & 1) == 0) {
+            float* r = red + (jl & 1) * (WC * 2 * kRows) + (warp * 2 + (q >> 1)) * kRows + 2 * g;
+            r[0] = c[0] + o2;
+            r[1] = c[1] + o3;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(b_idone + 8 * (jl & 1));
+    }
+}
+
+// ---- host side -------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+
+static bool make_plane_map(CUtensorMap* m, const uint8_t* planes, int n_max, int64_t rows, int64_t row_bytes) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)row_bytes, (cuuint64_t)rows, (cuuint64_t)n_max};
+    const cuuint64_t strides[2] = {(cuuint64_t)row_bytes, (cuuint64_t)(rows * row_bytes)};
+    const cuuint32_t box[3] = {128, (cuuint32_t)kRows, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)planes, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool make_lut_map(CUtensorMap* m, const uint16_t* lut, int k, int64_t rows) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    const int n = 1 << k, bx = n < 64 ? n : 64;
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)n * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)kRows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUtensorMapSwizzle sw =
+        k >= 6 ? CU_TENSOR_MAP_SWIZZLE_128B : (k == 5 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE);
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)lut, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (cached[dev] == 0) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+        cached[dev] = n;
+    }
+    return cached[dev];
+}
+
+constexpr size_t kSmemLimit = 227 * 1024;
+constexpr int kMaxStages = 8;
+
+template <int K>
+static int launch(Launch7& L, int flags, cudaStream_t s) {
+    using G = Geo<K>;
+    // ring depth: as many stages as fit (>= 3)
+    int nst = kMaxStages;
+    while (nst >= 3 && G::total(nst, L.xs_bytes) > kSmemLimit) --nst;
+    if (nst < 3) return -1;
+    L.n_stages = nst;
+    auto kern = gemv7_kernel<K>;
+    static std::atomic<int> configured{0};
+    if (!configured.load(std::memory_order_acquire)) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit) != cudaSuccess)
+            return APB_ERR_CUDA;
+        configured.store(1, std::memory_order_release);
+    }
+    int grid = sm_count();
+    if (grid > L.n_items) grid = L.n_items;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)G::kThreads);
+    cfg.dynamicSmemBytes = G::total(nst, L.xs_bytes);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (flags & APB_FLAG_PDL) ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, kern, L) != cudaSuccess) return APB_ERR_CUDA;
+    return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
+}
+
+}  // namespace apb7
+
+// Called by apb_gemv_grouped (apb_gemv.cu) after argument validation.
+// Returns -1 when this kernel does not apply (caller falls back), else a status.
+extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
+                             const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
+                             const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split,
+                             void* const* y, int y_dtype, const int64_t* ldy, int64_t y_off, int flags, void* stream) {
+    using namespace apb7;
+    static const bool disabled = [] {
+        const char* e = std::getenv("APB_GEMV_V7");
+        return e && e[0] == '0';
+    }();
+    if (disabled || k < 3 || k > 8 || m_x > 2 || n > kMaxProb) return -1;
+    static thread_local Launch7 L;  // ~5 KB: kept off the stack
+    std::memset(&L, 0, sizeof(L));
+    L.n_prob = n;
+    L.m_x = m_x;
+    L.x_split = x_split;
+    L.y_f16 = y_dtype == APB_DTYPE_F16;
+    int items = 0, max_tiles = 0;
+    int64_t cost = 0;
+    const int esz = y_dtype == APB_DTYPE_F16 ? 2 : 4;
+    for (int i = 0; i < n; ++i) {
+        Prob7& P = L.prob[i];
+        const int64_t row_bytes = padded[i] / 8;
+        if (!make_plane_map(&L.tm_planes[i], planes[i], n_max[i], rows[i], row_bytes)) return -1;
+        if (!make_lut_map(&L.tm_lut[i], lut[i], k, rows[i])) return -1;
+        P.x = x[i] + x_off * ldx[i];
+        P.y = reinterpret_cast<uint8_t*>(y[i]) + y_off * ldy[i] * esz;
+        P.rows = rows[i];
+        P.cols = cols[i];
+        P.ldx = ldx[i];
+        P.ldy = ldy[i];
+        P.n_tiles = (int)(padded[i] / kTileWeights);
+        P.item_begin = items;
+        P.cost_begin = cost;
+        const int ni = (int)((rows[i] + kRows - 1) / kRows);
+        items += ni;
+        cost += (int64_t)ni * P.n_tiles;
+        if (P.n_tiles > max_tiles) max_tiles = P.n_tiles;
+    }
+    L.n_items = items;
+    L.total_cost = cost;
+    L.xs_bytes = (int64_t)m_x * max_tiles * 2048;
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (k) {
+        case 3: return launch<3>(L, flags, s);
+        case 4: return launch<4>(L, flags, s);
+        case 5: return launch<5>(L, flags, s);
+        case 6: return launch<6>(L, flags, s);
+        case 7: return launch<7>(L, flags, s);
+        case 8: return launch<8>(L, flags, s);
+    }
+    return -1;
+}
