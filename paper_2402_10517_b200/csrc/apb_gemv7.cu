@@ -87,7 +87,7 @@ struct Geo {
     static constexpr int kLut = (kTableBytes + 1023) / 1024 * 1024;
     static constexpr int kRing = kLut + 2 * kLutSlot;
     static size_t total(int n_stages, int64_t xs_bytes) {
-        return (size_t)kRing + (size_t)n_stages * kStageBytes + 2 * (size_t)xs_bytes + kRedBytes + 256;
+        return (size_t)kRing + (size_t)n_stages * kStageBytes + 2 * (size_t)xs_bytes + kRedBytes + 16 * n_stages + 64;
     }
 };
 
@@ -138,6 +138,14 @@ __device__ __forceinline__ void lds128_keep(uint32_t& v0, uint32_t& v1, uint32_t
         "@p ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
         : "+r"(v0), "+r"(v1), "+r"(v2), "+r"(v3)
         : "r"(a), "r"(pred));
+}
+// B-fragment load from global (read-only path): only where pred != 0.
+__device__ __forceinline__ void ldg64_keep(uint32_t& v0, uint32_t& v1, const void* p, uint32_t pred) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
+        "@p ld.global.nc.v2.u32 {%0,%1}, [%2];\n\t}"
+        : "+r"(v0), "+r"(v1)
+        : "l"(p), "r"(pred));
 }
 __device__ __forceinline__ uint32_t u4w(const uint4& v, int i) {
     return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
@@ -224,8 +232,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
 
     const uint32_t s_lut = saddr(smem + G::kLut);
     const uint32_t s_ring = saddr(smem + G::kRing);
-    uint8_t* const xs = smem + G::kRing + (size_t)NST * G::kStageBytes;
-    float* const red = reinterpret_cast<float*>(xs + 2 * L.xs_bytes);
+    float* const red = reinterpret_cast<float*>(smem + G::kRing + (size_t)NST * G::kStageBytes);
     const uint32_t bar = saddr(reinterpret_cast<uint8_t*>(red) + G::kRedBytes);
     // barriers (8 B each): full[NST] | empty[NST] | lut_full[2] | lut_empty[2] | table_ready[2] | item_done[2]
     const uint32_t b_full = bar, b_empty = bar + 8 * NST, b_lfull = bar + 16 * NST, b_lempty = b_lfull + 16,
@@ -283,60 +290,61 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
     if (warp == WC + 1) {
         // ========================= service: tables, x, y =========================
         const int g = lane >> 2, q = lane & 3, rho = 2 * g + (q >> 1);
-        auto stage_x = [&](int pi, int xb) {
-            // [m][tile][t 32][half 2][p 4][4 halves]: 8-byte chunks, zero past cols
-            const Prob7& P = L.prob[pi];
-            const int chunks = L.m_x * P.n_tiles * 256;
-            const uint32_t base = saddr(xs + xb * L.xs_bytes);
-            for (int c = lane; c < chunks; c += 32) {
-                const int m = c / (P.n_tiles * 256), r = c - m * (P.n_tiles * 256);
-                const int tile = r >> 8, w = r & 255;
-                const int t = w >> 3, half = (w >> 2) & 1, p = w & 3;
-                const int64_t col = (int64_t)tile * kTileWeights + 256 * p + 8 * t + 4 * half;
-                const int64_t nb = (P.cols - col) * 2;
-                const uint16_t* src = P.x + (int64_t)m * P.ldx;
-                cp_async8(base + (uint32_t)(m * P.n_tiles * 2048 + r * 8), nb > 0 ? (const void*)(src + col) : (const void*)src,
-                          nb >= 8 ? 8 : (nb > 0 ? (int)nb : 0));
-            }
-            asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
-        };
         auto build = [&](int slot) {
-            // this lane's table column: row rho, copy q & 1 -> [entry][slot][lane]
+            // table[entry][slot][lane]: lanes 4g..4g+3 = (row 2g, 2g, 2g+1, 2g+1) -> one
+            // 16-byte store per (entry, g) holds both copies of both rows.  Lane
+            // (e4 = lane >> 3, gg = lane & 7) writes entries e = e4 (mod 4) of rows 2gg, 2gg+1.
+            const int e4 = lane >> 3, gg = lane & 7, r0 = 2 * gg, r1 = r0 + 1;
             const uint32_t lut = s_lut + slot * G::kLutSlot;
-            const uint32_t dst = saddr(smem) + slot * 128 + lane * 4;
+            const uint32_t dst = saddr(smem) + slot * 128 + gg * 16;
             if constexpr (G::kPair) {
-                uint32_t h[1 << K];
-                if constexpr (K == 3) {
-                    const uint4 v = lds128(lut + rho * 16);
-                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                uint32_t h0[1 << K], h1[1 << K];
+                constexpr int RB = (1 << K) * 2;  // LUT row bytes (16 or 32)
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) h[i] = (i & 1) ? (w4[i >> 1] >> 16) : (w4[i >> 1] & 0xFFFFu);
-                } else {  // K == 4: 32-byte rows
-                    const uint4 v0 = lds128(lut + rho * 32), v1 = lds128(lut + rho * 32 + 16);
-                    const uint32_t w8[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) h[i] = (i & 1) ? (w8[i >> 1] >> 16) : (w8[i >> 1] & 0xFFFFu);
-                }
-#pragma unroll
-                for (int idx = 0; idx < G::kEntries; ++idx) {
-                    uint32_t ce, co;
-                    apb::pair_codes<K>((uint32_t)idx, ce, co);
-                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(dst + idx * 256), "r"(h[ce] | (h[co] << 16)) : "memory");
-                }
-            } else {
-#pragma unroll 4
-                for (int cc = 0; cc < G::kLutHalves / 8; ++cc) {
-                    // 16-byte chunk cc of row rho (box layout + swizzle of the LUT map)
-                    const int b = cc / 8, ci = cc % 8;
-                    uint32_t a;
-                    if constexpr (K == 5) a = rho * 64 + ((ci ^ ((rho >> 1) & 3)) << 4);
-                    else a = b * (kRows * 128) + rho * 128 + ((ci ^ (rho & 7)) << 4);
-                    const uint4 v = lds128(lut + a);
-                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                for (int c = 0; c < RB / 16; ++c) {
+                    const uint4 v0 = lds128(lut + r0 * RB + c * 16), v1 = lds128(lut + r1 * RB + c * 16);
+                    const uint32_t a0[4] = {v0.x, v0.y, v0.z, v0.w}, a1[4] = {v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const uint32_t e = (i & 1) ? (w4[i >> 1] >> 16) : (w4[i >> 1] & 0xFFFFu);
-                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(dst + (cc * 8 + i) * 256), "r"(e) : "memory");
+                        h0[c * 8 + i] = (i & 1) ? (a0[i >> 1] >> 16) : (a0[i >> 1] & 0xFFFFu);
+                        h1[c * 8 + i] = (i & 1) ? (a1[i >> 1] >> 16) : (a1[i >> 1] & 0xFFFFu);
+                    }
+                }
+                // idx = 4i + e4: pair-index bits 0/1 (= code bit 0 of the even / odd
+                // column) come from e4, the rest from i (compile time)
+                constexpr int NH = 1 << (K - 1);
+                uint32_t s0[NH], s1[NH], o0[NH], o1[NH];
+#pragma unroll
+                for (int c = 0; c < NH; ++c) {
+                    s0[c] = (e4 & 1) ? h0[2 * c + 1] : h0[2 * c];
+                    s1[c] = (e4 & 1) ? h1[2 * c + 1] : h1[2 * c];
+                    o0[c] = (e4 & 2) ? h0[2 * c + 1] : h0[2 * c];
+                    o1[c] = (e4 & 2) ? h1[2 * c + 1] : h1[2 * c];
+                }
+#pragma unroll
+                for (int i = 0; i < G::kEntries / 4; ++i) {
+                    uint32_t ce, co;
+                    apb::pair_codes<K - 1>((uint32_t)i, ce, co);
+                    const uint32_t v0 = s0[ce] | (o0[co] << 16), v1 = s1[ce] | (o1[co] << 16);
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%2,%2};" ::"r"(dst + (4 * i + e4) * 256), "r"(v0), "r"(v1)
+                                 : "memory");
+                }
+            } else {
+                auto chunk_addr = [&](int r, int cc) -> uint32_t {  // 16-byte chunk cc of LUT row r
+                    const int b = cc / 8, ci = cc % 8;
+                    if constexpr (K == 5) return lut + r * 64 + ((ci ^ ((r >> 1) & 3)) << 4);
+                    else return lut + b * (kRows * 128) + r * 128 + ((ci ^ (r & 7)) << 4);
+                };
+#pragma unroll 2
+                for (int cc = e4; cc < G::kLutHalves / 8; cc += 4) {
+                    const uint4 v0 = lds128(chunk_addr(r0, cc)), v1 = lds128(chunk_addr(r1, cc));
+                    const uint32_t a0[4] = {v0.x, v0.y, v0.z, v0.w}, a1[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const uint32_t x0 = (i & 1) ? (a0[i >> 1] >> 16) : (a0[i >> 1] & 0xFFFFu);
+                        const uint32_t x1 = (i & 1) ? (a1[i >> 1] >> 16) : (a1[i >> 1] & 0xFFFFu);
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%1,%2,%2};" ::"r"(dst + (cc * 8 + i) * 256), "r"(x0), "r"(x1)
+                                     : "memory");
                     }
                 }
             }
@@ -370,32 +378,31 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
             }
         };
 
+        // tables depend only on the weights: they are built before the previous
+        // kernel of the stream has finished (PDL); y is written only after it has
         int pi = problem_of(L, first), pend = problem_end(L, pi);
-        int xb = 0, pi_hist[2] = {pi, pi};
+        int pi_hist[2] = {pi, pi};
 #pragma unroll 1
         for (int jl = 0; jl < n_local + 2; ++jl) {
             if (jl >= 2) {  // item jl-2 done by every compute warp: reduce it, free its slot
                 mbar_wait(b_idone + 8 * (jl & 1), ((jl - 2) >> 1) & 1);
+                if (jl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
                 reduce(first + jl - 2, pi_hist[jl & 1], jl & 1);
             }
             if (jl < n_local) {
                 const int item = first + jl;
-                bool new_x = jl == 0;
                 if (item >= pend) {
                     pi = problem_of(L, item);
                     pend = problem_end(L, pi);
-                    xb ^= 1;
-                    new_x = true;
                 }
                 pi_hist[jl & 1] = pi;
                 mbar_wait(b_lfull + 8 * (jl & 1), (jl >> 1) & 1);
                 build(jl & 1);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(b_lempty + 8 * (jl & 1));
-                if (jl == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // x / y of earlier kernels
-                if (new_x) stage_x(pi, xb);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(b_tready + 8 * (jl & 1));
+                if (lane == 0) {
+                    mbar_arrive(b_lempty + 8 * (jl & 1));
+                    mbar_arrive(b_tready + 8 * (jl & 1));
+                }
             }
         }
         return;
@@ -407,16 +414,18 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
     const int grp = warp >> 2, su = warp & 3;
     const int ch = su + 4 * cp;  // 16-byte chunk of the tile row: words 4ch .. 4ch+3
     const uint32_t plane_off = rho * 128 + ((ch ^ (rho & 7)) << 4);  // 128B-swizzled stage row
-    // B fragment role: column n = g; batch row m = g >> 2, set = (g >> 1) & 1
+    // B fragment role: column n = g; batch row m = g >> 2, set = (g >> 1) & 1.
+    // Live lanes read x[m][tile*1024 + 256p + 8t + 4*set + 0..3] (8 bytes) straight
+    // from global memory (read-only path, L1/L2 resident); the others keep zeros.
     const int gm = g >> 2, gset = (g >> 1) & 1;
     const uint32_t xlive = (gm < L.m_x && (q >> 1) == (g & 1)) ? 1u : 0u;
-    const uint32_t x_lane = (uint32_t)(4 * ch) * 64u + (uint32_t)gset * 32u;  // + tile*2048 + wi*64 + {0,16}
+    const int xcol_lane = 8 * (4 * ch) + 4 * gset;  // + tile*1024 + 256p + 8wi
 
     uint32_t xr[2][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) xr[0][i] = xr[1][i] = 0u;
 
-    int pi = problem_of(L, first), pend = problem_end(L, pi), xb = 0;
+    int pi = problem_of(L, first), pend = problem_end(L, pi);
     int gs = grp;           // next ring stage of this warp group
     int item_gs = 0;        // first stage of the current item
 #pragma unroll 1
@@ -425,16 +434,18 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
         if (item >= pend) {
             pi = problem_of(L, item);
             pend = problem_end(L, pi);
-            xb ^= 1;
         }
-        const int nt = L.prob[pi].n_tiles;
-        const uint32_t xrow = saddr(xs + xb * L.xs_bytes) + (uint32_t)gm * (uint32_t)(nt * 2048) + x_lane;
+        const Prob7& P = L.prob[pi];
+        const int nt = P.n_tiles;
+        const uint16_t* const xrow = P.x + (int64_t)(gm < L.m_x ? gm : 0) * P.ldx + xcol_lane;
+        const int64_t xcols = P.cols - xcol_lane;  // column limit relative to xrow
         const uint32_t off = (uint32_t)(jl & 1) * 128u + (uint32_t)lane * 4u;
         float acc[2][4];
 #pragma unroll
         for (int c2 = 0; c2 < 2; ++c2) acc[c2][0] = acc[c2][1] = acc[c2][2] = acc[c2][3] = 0.f;
 
-        mbar_wait(b_tready + 8 * (jl & 1), (jl >> 1) & 1);  // table (and x) of this item
+        mbar_wait(b_tready + 8 * (jl & 1), (jl >> 1) & 1);  // table of this item
+        if (jl == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // x may come from the previous kernel
 #pragma unroll 1
         for (; gs < item_gs + nt; gs += NG) {
             const int tile = gs - item_gs;
@@ -444,12 +455,25 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
             uint4 pv[K];
 #pragma unroll
             for (int p = 0; p < K; ++p) pv[K - 1 - p] = lds128(sb + p * 2048);  // Q[i] = plane K-1-i (LSB first)
-            const uint32_t xa = xrow + (uint32_t)tile * 2048u;
+            const uint16_t* const xa = xrow + tile * kTileWeights;
+            const bool xfull = (int64_t)(tile + 1) * kTileWeights <= P.cols;
 #pragma unroll
             for (int wi = 0; wi < 4; ++wi) {
                 uint32_t(&xv)[8] = xr[wi & 1];
-                lds128_keep(xv[0], xv[1], xv[2], xv[3], xa + wi * 64, xlive);
-                lds128_keep(xv[4], xv[5], xv[6], xv[7], xa + wi * 64 + 16, xlive);
+                if (xfull) {
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) ldg64_keep(xv[2 * p], xv[2 * p + 1], xa + 256 * p + 8 * wi, xlive);
+                } else if (xlive) {  // tail tile: zero past cols
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                        const int64_t c0 = (int64_t)tile * kTileWeights + 256 * p + 8 * wi;
+                        uint32_t h[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) h[i] = c0 + i < xcols ? (uint32_t)__ldg(xa + 256 * p + 8 * wi + i) : 0u;
+                        xv[2 * p] = h[0] | (h[1] << 16);
+                        xv[2 * p + 1] = h[2] | (h[3] << 16);
+                    }
+                }
                 uint32_t Q[K];
 #pragma unroll
                 for (int i = 0; i < K; ++i) Q[i] = u4w(pv[i], wi);
@@ -536,7 +560,7 @@ static int sm_count() {
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 16;
 
 template <int K>
 static int launch(Launch7& L, int flags, cudaStream_t s) {
@@ -613,7 +637,7 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     }
     L.n_items = items;
     L.total_cost = cost;
-    L.xs_bytes = (int64_t)m_x * max_tiles * 2048;
+    L.xs_bytes = 0;  // activations are read from global memory
     cudaStream_t s = (cudaStream_t)stream;
     switch (k) {
         case 3: return launch<3>(L, flags, s);
