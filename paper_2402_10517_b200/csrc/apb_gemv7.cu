@@ -47,6 +47,11 @@ using apb::prmt;
 constexpr int kRows = 16;      // rows per item
 constexpr int kMaxProb = 16;   // problems per grouped launch
 constexpr int kSmemBase = 1024;  // sm_100 reserves the first 1 KB of the shared window
+constexpr int kMaxCols = 64 * 1024;  // padded columns per layer on this path
+
+// Zero activations: B-fragment lanes that must hold zeros read from here, so
+// every lane issues the same unpredicated load (no divergence).
+__device__ __align__(16) uint16_t g_zero_x[kMaxCols];
 
 struct Prob7 {
     const uint16_t* x;  // fp16 [m_x][ldx]
@@ -87,7 +92,7 @@ struct Geo {
     static constexpr int kLut = (kTableBytes + 1023) / 1024 * 1024;
     static constexpr int kRing = kLut + 2 * kLutSlot;
     static size_t total(int n_stages, int64_t xs_bytes) {
-        return (size_t)kRing + (size_t)n_stages * kStageBytes + 2 * (size_t)xs_bytes + kRedBytes + 16 * n_stages + 64;
+        return (size_t)kRing + (size_t)n_stages * kStageBytes + 2 * (size_t)xs_bytes + kRedBytes + 16 * n_stages + 96;
     }
 };
 
@@ -111,6 +116,33 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
         "@!p bra W_%=;\n\t}" ::"r"(a),
         "r"(parity)
         : "memory");
+}
+// try_wait with a suspend-time hint: a waiting warp sleeps in the barrier unit
+// instead of spinning through issue slots other warps could use.
+__device__ __forceinline__ void mbar_sleep(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra S_%=;\n\t}" ::"r"(a),
+        "r"(parity), "r"(1000000)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void lds64_keep(uint32_t& v0, uint32_t& v1, uint32_t a, uint32_t pred) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
+        "@p ld.shared.v2.u32 {%0,%1}, [%2];\n\t}"
+        : "+r"(v0), "+r"(v1)
+        : "r"(a), "r"(pred));
 }
 __device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, uint32_t bar) {
     asm volatile(
@@ -232,11 +264,12 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
 
     const uint32_t s_lut = saddr(smem + G::kLut);
     const uint32_t s_ring = saddr(smem + G::kRing);
-    float* const red = reinterpret_cast<float*>(smem + G::kRing + (size_t)NST * G::kStageBytes);
+    uint8_t* const xs = smem + G::kRing + (size_t)NST * G::kStageBytes;  // [2][m_x][padded] fp16
+    float* const red = reinterpret_cast<float*>(xs + 2 * L.xs_bytes);
     const uint32_t bar = saddr(reinterpret_cast<uint8_t*>(red) + G::kRedBytes);
-    // barriers (8 B each): full[NST] | empty[NST] | lut_full[2] | lut_empty[2] | table_ready[2] | item_done[2]
+    // barriers (8 B each): full[NST] | empty[NST] | lut_full[2] | lut_empty[2] | table_ready[2] | item_done[2] | x_full[2]
     const uint32_t b_full = bar, b_empty = bar + 8 * NST, b_lfull = bar + 16 * NST, b_lempty = b_lfull + 16,
-                   b_tready = b_lfull + 32, b_idone = b_lfull + 48;
+                   b_tready = b_lfull + 32, b_idone = b_lfull + 48, b_xfull = b_lfull + 64;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(b_full + 8 * i, 1);
@@ -247,6 +280,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
             mbar_init(b_lempty + 8 * i, 1);
             mbar_init(b_tready + 8 * i, 1);
             mbar_init(b_idone + 8 * i, WC);
+            mbar_init(b_xfull + 8 * i, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -255,7 +289,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
     if (warp == WC) {
         // ============================ producer (TMA) ============================
         if (lane != 0) return;
-        int gs = 0;
+        int slot = 0, ph = 0;  // ring position of the next stage
         int pi = problem_of(L, first), pend = problem_end(L, pi);
 #pragma unroll 1
         for (int jl = 0; jl < n_local; ++jl) {
@@ -275,13 +309,16 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
                      b_lfull + 8 * (jl & 1));
             // plane tiles -> ring stages
 #pragma unroll 1
-            for (int t = 0; t < P.n_tiles; ++t, ++gs) {
-                const int slot = gs % NST, ph = gs / NST;
+            for (int t = 0; t < P.n_tiles; ++t) {
                 if (ph > 0) mbar_wait(b_empty + 8 * slot, (ph - 1) & 1);
                 mbar_expect_tx(b_full + 8 * slot, G::kStageBytes);
                 const uint32_t dst = s_ring + slot * G::kStageBytes;
 #pragma unroll
                 for (int p = 0; p < K; ++p) tma3(dst + p * 2048, &L.tm_planes[pi], t * kTileBytes, row0, p, b_full + 8 * slot);
+                if (++slot == NST) {
+                    slot = 0;
+                    ++ph;
+                }
             }
         }
         return;
@@ -380,20 +417,34 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
 
         // tables depend only on the weights: they are built before the previous
         // kernel of the stream has finished (PDL); y is written only after it has
-        int pi = problem_of(L, first), pend = problem_end(L, pi);
+        // activations of problem pi -> x buffer xb (one bulk copy per batch row;
+        // columns past cols are masked by the compute warps)
+        auto issue_x = [&](int pi, int xb) {
+            if (lane != 0) return;
+            const Prob7& P = L.prob[pi];
+            const uint32_t bytes = (uint32_t)((P.cols + 7) / 8 * 16);
+            mbar_expect_tx(b_xfull + 8 * xb, bytes * L.m_x);
+            for (int m = 0; m < L.m_x; ++m)
+                bulk_g2s(saddr(xs + xb * L.xs_bytes) + m * P.n_tiles * 2048, P.x + (int64_t)m * P.ldx, bytes,
+                         b_xfull + 8 * xb);
+        };
+        // tables depend only on the weights: they are built before the previous
+        // kernel of the stream has finished (PDL); x is read and y written after
+        int pi = problem_of(L, first), pend = problem_end(L, pi), xb = 0;
         int pi_hist[2] = {pi, pi};
 #pragma unroll 1
         for (int jl = 0; jl < n_local + 2; ++jl) {
             if (jl >= 2) {  // item jl-2 done by every compute warp: reduce it, free its slot
                 mbar_wait(b_idone + 8 * (jl & 1), ((jl - 2) >> 1) & 1);
-                if (jl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
                 reduce(first + jl - 2, pi_hist[jl & 1], jl & 1);
             }
             if (jl < n_local) {
                 const int item = first + jl;
-                if (item >= pend) {
+                if (item >= pend) {  // next layer of a grouped launch (its x goes to the other buffer)
                     pi = problem_of(L, item);
                     pend = problem_end(L, pi);
+                    xb ^= 1;
+                    issue_x(pi, xb);
                 }
                 pi_hist[jl & 1] = pi;
                 mbar_wait(b_lfull + 8 * (jl & 1), (jl >> 1) & 1);
@@ -403,89 +454,115 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
                     mbar_arrive(b_lempty + 8 * (jl & 1));
                     mbar_arrive(b_tready + 8 * (jl & 1));
                 }
+                if (jl == 0) {
+                    asm volatile("griddepcontrol.wait;" ::: "memory");  // x / y of earlier kernels
+                    issue_x(pi, 0);
+                }
             }
         }
         return;
     }
 
     // =============================== compute warps ===============================
+    // Lane (g, q): row rho = 2g + (q >> 1) of the item, copy cp = q & 1.  Warp su
+    // = warp & 3 of its group takes 16-byte chunks su and su + 4 of every stage
+    // (tile) row; copy cp reads words 2cp, 2cp+1 of a chunk (LDS.64: rows 0..7 of a
+    // phase hit 8 distinct swizzled chunks).  Word t = 4ch + 2cp + wi.
     const int g = lane >> 2, q = lane & 3;
     const int rho = 2 * g + (q >> 1), cp = q & 1;
     const int grp = warp >> 2, su = warp & 3;
-    const int ch = su + 4 * cp;  // 16-byte chunk of the tile row: words 4ch .. 4ch+3
-    const uint32_t plane_off = rho * 128 + ((ch ^ (rho & 7)) << 4);  // 128B-swizzled stage row
-    // B fragment role: column n = g; batch row m = g >> 2, set = (g >> 1) & 1.
-    // Live lanes read x[m][tile*1024 + 256p + 8t + 4*set + 0..3] (8 bytes) straight
-    // from global memory (read-only path, L1/L2 resident); the others keep zeros.
+    uint32_t plane_off[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) plane_off[j] = rho * 128 + (((su + 4 * j) ^ (rho & 7)) << 4) + cp * 8;
+    // B fragment role: column n = g; batch row gm = g >> 2, column set gset = (g >> 1) & 1.
+    // Live lanes read x[gm][tile*1024 + 256p + 8t + 4*gset .. +3] (8 bytes, raw
+    // layout: the 4 live addresses of a load are 8/32 B apart -> one wavefront);
+    // the others keep zeros.
     const int gm = g >> 2, gset = (g >> 1) & 1;
     const uint32_t xlive = (gm < L.m_x && (q >> 1) == (g & 1)) ? 1u : 0u;
-    const int xcol_lane = 8 * (4 * ch) + 4 * gset;  // + tile*1024 + 256p + 8wi
+    const int xcol_lane = 32 * su + 4 * cp + 4 * gset;  // + tile*1024 + 256p + 128j + 8wi (+4cp via 2cp words)
 
-    uint32_t xr[2][8];
+    uint32_t xv[2][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) xr[0][i] = xr[1][i] = 0u;
+    for (int i = 0; i < 8; ++i) xv[0][i] = xv[1][i] = 0u;
 
-    int pi = problem_of(L, first), pend = problem_end(L, pi);
-    int gs = grp;           // next ring stage of this warp group
-    int item_gs = 0;        // first stage of the current item
+    int pi = problem_of(L, first), pend = problem_end(L, pi), xb = 0, xph[2] = {0, 0};
+    int gs = grp;            // next ring stage of this warp group
+    int item_gs = 0;         // first stage of the current item
+    int slot = grp, ph = 0;  // ring slot / phase parity of stage gs (NST >= NG)
 #pragma unroll 1
     for (int jl = 0; jl < n_local; ++jl) {
         const int item = first + jl;
+        bool new_x = jl == 0;
         if (item >= pend) {
             pi = problem_of(L, item);
             pend = problem_end(L, pi);
+            xb ^= 1;
+            new_x = true;
         }
         const Prob7& P = L.prob[pi];
         const int nt = P.n_tiles;
-        const uint16_t* const xrow = P.x + (int64_t)(gm < L.m_x ? gm : 0) * P.ldx + xcol_lane;
-        const int64_t xcols = P.cols - xcol_lane;  // column limit relative to xrow
+        // column of word t = 4ch + 2cp + wi: 8t = 32su + 128j + 16cp + 8wi
+        const int xcol0 = 32 * su + 16 * cp + 4 * gset;
+        const uint32_t xrow = saddr(xs + xb * L.xs_bytes) + (uint32_t)(gm < L.m_x ? gm : 0) * (uint32_t)(nt * 2048) +
+                              (uint32_t)xcol0 * 2u;
+        const int64_t xcols = P.cols - xcol0;  // column limit relative to xrow
+        const int full_tiles = (int)(P.cols / kTileWeights);
         const uint32_t off = (uint32_t)(jl & 1) * 128u + (uint32_t)lane * 4u;
         float acc[2][4];
 #pragma unroll
         for (int c2 = 0; c2 < 2; ++c2) acc[c2][0] = acc[c2][1] = acc[c2][2] = acc[c2][3] = 0.f;
 
-        mbar_wait(b_tready + 8 * (jl & 1), (jl >> 1) & 1);  // table of this item
-        if (jl == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // x may come from the previous kernel
+        mbar_sleep(b_tready + 8 * (jl & 1), (jl >> 1) & 1);  // table of this item
+        if (new_x) {  // activations of this layer staged
+            mbar_sleep(b_xfull + 8 * xb, xph[xb]);
+            xph[xb] ^= 1;
+        }
 #pragma unroll 1
         for (; gs < item_gs + nt; gs += NG) {
             const int tile = gs - item_gs;
-            const int slot = gs % NST, ph = gs / NST;
-            mbar_wait(b_full + 8 * slot, ph & 1);
-            const uint32_t sb = s_ring + slot * G::kStageBytes + plane_off;
-            uint4 pv[K];
+            mbar_sleep(b_full + 8 * slot, ph);
+            const uint32_t sb = s_ring + slot * G::kStageBytes;
+            const uint32_t xa = xrow + (uint32_t)tile * 2048u;
+            const bool xfull = tile < full_tiles;
 #pragma unroll
-            for (int p = 0; p < K; ++p) pv[K - 1 - p] = lds128(sb + p * 2048);  // Q[i] = plane K-1-i (LSB first)
-            const uint16_t* const xa = xrow + tile * kTileWeights;
-            const bool xfull = (int64_t)(tile + 1) * kTileWeights <= P.cols;
+            for (int j = 0; j < 2; ++j) {
+                uint2 pv[K];
 #pragma unroll
-            for (int wi = 0; wi < 4; ++wi) {
-                uint32_t(&xv)[8] = xr[wi & 1];
-                if (xfull) {
+                for (int p = 0; p < K; ++p) pv[K - 1 - p] = lds64(sb + p * 2048 + plane_off[j]);  // Q[i] = plane K-1-i
 #pragma unroll
-                    for (int p = 0; p < 4; ++p) ldg64_keep(xv[2 * p], xv[2 * p + 1], xa + 256 * p + 8 * wi, xlive);
-                } else if (xlive) {  // tail tile: zero past cols
+                for (int wi = 0; wi < 2; ++wi) {
+                    uint32_t(&x8)[8] = xv[wi];
+                    const uint32_t xo = (uint32_t)(256 * j + 16 * wi);  // bytes: 128j + 8wi columns
 #pragma unroll
-                    for (int p = 0; p < 4; ++p) {
-                        const int64_t c0 = (int64_t)tile * kTileWeights + 256 * p + 8 * wi;
-                        uint32_t h[4];
+                    for (int p = 0; p < 4; ++p) lds64_keep(x8[2 * p], x8[2 * p + 1], xa + xo + 512 * p, xlive);
+                    if (!xfull) {  // tail tile: columns >= cols are zero
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) h[i] = c0 + i < xcols ? (uint32_t)__ldg(xa + 256 * p + 8 * wi + i) : 0u;
-                        xv[2 * p] = h[0] | (h[1] << 16);
-                        xv[2 * p + 1] = h[2] | (h[3] << 16);
+                        for (int p = 0; p < 4; ++p) {
+                            const int64_t c0 = (int64_t)tile * kTileWeights + 256 * p + 128 * j + 8 * wi;
+                            x8[2 * p] &= (c0 < xcols ? 0x0000FFFFu : 0u) | (c0 + 1 < xcols ? 0xFFFF0000u : 0u);
+                            x8[2 * p + 1] &= (c0 + 2 < xcols ? 0x0000FFFFu : 0u) | (c0 + 3 < xcols ? 0xFFFF0000u : 0u);
+                        }
                     }
-                }
-                uint32_t Q[K];
+                    uint32_t Q[K];
 #pragma unroll
-                for (int i = 0; i < K; ++i) Q[i] = u4w(pv[i], wi);
-                uint32_t a[16];
-                decode_word<K>(Q, off, a);
-                if (wi == 0) {  // every plane register has been consumed: release the stage
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(b_empty + 8 * slot);
-                }
+                    for (int i = 0; i < K; ++i) Q[i] = wi ? pv[i].y : pv[i].x;
+                    uint32_t a[16];
+                    decode_word<K>(Q, off, a);
+                    if (j == 1 && wi == 0) {  // every plane register of the stage consumed: release it
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(b_empty + 8 * slot);
+                        slot += NG;
+                        if (slot >= NST) {
+                            slot -= NST;
+                            ph ^= 1;
+                        }
+                    }
 #pragma unroll
-                for (int p = 0; p < 4; ++p)
-                    mma16816(acc[p & 1], a[p * 4 + 0], a[p * 4 + 2], a[p * 4 + 1], a[p * 4 + 3], xv[2 * p], xv[2 * p + 1]);
+                    for (int p = 0; p < 4; ++p)
+                        mma16816(acc[p & 1], a[p * 4 + 0], a[p * 4 + 2], a[p * 4 + 1], a[p * 4 + 3], x8[2 * p],
+                                 x8[2 * p + 1]);
+                }
             }
         }
         item_gs += nt;
@@ -567,8 +644,8 @@ static int launch(Launch7& L, int flags, cudaStream_t s) {
     using G = Geo<K>;
     // ring depth: as many stages as fit (>= 3)
     int nst = kMaxStages;
-    while (nst >= 3 && G::total(nst, L.xs_bytes) > kSmemLimit) --nst;
-    if (nst < 3) return -1;
+    while (nst >= G::kNG && G::total(nst, L.xs_bytes) > kSmemLimit) --nst;
+    if (nst < G::kNG || nst < 3) return -1;
     L.n_stages = nst;
     auto kern = gemv7_kernel<K>;
     static std::atomic<int> configured{0};
@@ -607,6 +684,8 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
         return e && e[0] == '0';
     }();
     if (disabled || k < 3 || k > 8 || m_x > 2 || n > kMaxProb) return -1;
+    for (int i = 0; i < n; ++i)
+        if (padded[i] > kMaxCols) return -1;
     static thread_local Launch7 L;  // ~5 KB: kept off the stack
     std::memset(&L, 0, sizeof(L));
     L.n_prob = n;
@@ -637,7 +716,7 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     }
     L.n_items = items;
     L.total_cost = cost;
-    L.xs_bytes = 0;  // activations are read from global memory
+    L.xs_bytes = (int64_t)m_x * max_tiles * 2048;
     cudaStream_t s = (cudaStream_t)stream;
     switch (k) {
         case 3: return launch<3>(L, flags, s);
