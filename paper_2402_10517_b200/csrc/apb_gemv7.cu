@@ -273,13 +273,13 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(b_full + 8 * i, 1);
-            mbar_init(b_empty + 8 * i, 4);
+            mbar_init(b_empty + 8 * i, 4 * 32);  // every lane of the 4 consumer warps arrives
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(b_lfull + 8 * i, 1);
             mbar_init(b_lempty + 8 * i, 1);
             mbar_init(b_tready + 8 * i, 1);
-            mbar_init(b_idone + 8 * i, WC);
+            mbar_init(b_idone + 8 * i, WC * 32);
             mbar_init(b_xfull + 8 * i, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -550,8 +550,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
                     uint32_t a[16];
                     decode_word<K>(Q, off, a);
                     if (j == 1 && wi == 0) {  // every plane register of the stage consumed: release it
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(b_empty + 8 * slot);
+                        mbar_arrive(b_empty + 8 * slot);
                         slot += NG;
                         if (slot >= NST) {
                             slot -= NST;
@@ -576,8 +575,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
             r[0] = c[0] + o2;
             r[1] = c[1] + o3;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(b_idone + 8 * (jl & 1));
+        mbar_arrive(b_idone + 8 * (jl & 1));  // all lanes (release orders the partial stores)
     }
 }
 
