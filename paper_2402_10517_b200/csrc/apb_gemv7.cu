@@ -53,6 +53,21 @@ constexpr int kMaxCols = 64 * 1024;  // padded columns per layer on this path
 // every lane issues the same unpredicated load (no divergence).
 __device__ __align__(16) uint16_t g_zero_x[kMaxCols];
 
+#ifdef APB_TIMELINE
+// Debug builds (tools/kbench timeline): per-CTA globaltimer stamps (ns).
+__device__ unsigned long long g_tl7[1024 * 8];
+__device__ __forceinline__ void tl_stamp(int i) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tl7[blockIdx.x * 8 + i] = t;
+}
+#define APB_TL(i) tl_stamp(i)
+#else
+#define APB_TL(i) \
+    do {          \
+    } while (0)
+#endif
+
 struct Prob7 {
     const uint16_t* x;  // fp16 [m_x][ldx]
     void* y;            // [m_out][ldy]
@@ -84,7 +99,11 @@ struct Geo {
     static constexpr int kLutBytes = kRows * kLutHalves * 2;
     static constexpr int kLutSlot = (kLutBytes + 1023) / 1024 * 1024;
     static constexpr int kStageBytes = K * 2048;  // 16 rows x 128 B x K planes
-    static constexpr int kWC = 12;                // compute warps: 3 groups of 4
+#ifdef APB7_WC
+    static constexpr int kWC = APB7_WC;
+#else
+    static constexpr int kWC = K == 8 ? 12 : 16;  // compute warps, groups of 4 (measured best per k)
+#endif
     static constexpr int kNG = kWC / 4;
     static constexpr int kThreads = (kWC + 2) * 32;
     static constexpr int kRedBytes = 2 * kWC * 2 * kRows * 4;  // [slot][warp][m][row] f32
@@ -259,6 +278,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
     const int last = item_at_cost(L, L.total_cost * (int64_t)(blockIdx.x + 1) / gridDim.x);
     asm volatile("griddepcontrol.launch_dependents;");
     if (first >= last) return;
+    if (tid == 0) APB_TL(0);
     const int n_local = last - first;
     const int NST = L.n_stages;
 
@@ -321,6 +341,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
                 }
             }
         }
+        APB_TL(6);
         return;
     }
 
@@ -432,6 +453,12 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
         // kernel of the stream has finished (PDL); x is read and y written after
         int pi = problem_of(L, first), pend = problem_end(L, pi), xb = 0;
         int pi_hist[2] = {pi, pi};
+        // x of the first layer: its bulk copy overlaps the centroid-row / plane
+        // latency of the first item.  (A CTA of this kernel only becomes resident
+        // once the previous kernel's CTAs leave the SM, so the PDL wait is short.)
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // x / y of earlier kernels
+        issue_x(pi, 0);
+        if (lane == 0) APB_TL(2);
 #pragma unroll 1
         for (int jl = 0; jl < n_local + 2; ++jl) {
             if (jl >= 2) {  // item jl-2 done by every compute warp: reduce it, free its slot
@@ -454,12 +481,10 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
                     mbar_arrive(b_lempty + 8 * (jl & 1));
                     mbar_arrive(b_tready + 8 * (jl & 1));
                 }
-                if (jl == 0) {
-                    asm volatile("griddepcontrol.wait;" ::: "memory");  // x / y of earlier kernels
-                    issue_x(pi, 0);
-                }
+                if (jl == 0 && lane == 0) APB_TL(1);
             }
         }
+        if (lane == 0) APB_TL(5);
         return;
     }
 
@@ -522,6 +547,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
         for (; gs < item_gs + nt; gs += NG) {
             const int tile = gs - item_gs;
             mbar_sleep(b_full + 8 * slot, ph);
+            if (warp == 0 && lane == 0 && gs == 0) APB_TL(3);
             const uint32_t sb = s_ring + slot * G::kStageBytes;
             const uint32_t xa = xrow + (uint32_t)tile * 2048u;
             const bool xfull = tile < full_tiles;
@@ -576,6 +602,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
             r[1] = c[1] + o3;
         }
         mbar_arrive(b_idone + 8 * (jl & 1));  // all lanes (release orders the partial stores)
+        if (warp == 0 && lane == 0 && jl == 0) APB_TL(4);
     }
 }
 
@@ -672,6 +699,12 @@ static int launch(Launch7& L, int flags, cudaStream_t s) {
 
 // Called by apb_gemv_grouped (apb_gemv.cu) after argument validation.
 // Returns -1 when this kernel does not apply (caller falls back), else a status.
+#ifdef APB_TIMELINE
+extern "C" int apb7_read_timeline(unsigned long long* host, int n) {
+    return cudaMemcpyFromSymbol(host, apb7::g_tl7, sizeof(unsigned long long) * 8 * n) == cudaSuccess ? 0 : 5;
+}
+#endif
+
 extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
                              const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
                              const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split,
