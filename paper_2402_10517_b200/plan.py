@@ -73,6 +73,18 @@ class GemvPlan:
         self._ldy = int64_array([t.rows for t in ts])
         self._lib = load()
 
+    def rebind(self, x_list, y_list):
+        """Point the plan at caller-owned device activation / output buffers
+        (same shapes and dtypes as the ones it allocated)."""
+        if len(x_list) != len(self.x) or len(y_list) != len(self.y):
+            raise ParameterError("rebind needs one x and one y per layer")
+        for old, new in list(zip(self.x, x_list)) + list(zip(self.y, y_list)):
+            if tuple(old.shape) != tuple(new.shape) or old.dtype != new.dtype or not new.is_cuda:
+                raise ParameterError("rebind buffers must match the plan's shapes and dtypes")
+        self.x, self.y = list(x_list), list(y_list)
+        self._xp = ptr_array([dev.ptr(x) for x in self.x])
+        self._yp = ptr_array([dev.ptr(y) for y in self.y])
+
     def algorithmic_bytes(self) -> int:
         """R*C*k/8 (unpadded top-k planes) + R*2^k*2 (fp16
         LUT) + M*C*2 (fp16 x) + M*R*2 (fp16 y), summed over the layers."""
@@ -115,3 +127,80 @@ class GemvPlan:
             for _ in range(repeats):
                 self.run()
         return g
+
+
+class StepPlan:
+    """A decode step: a fixed sequence of ``GemvPlan`` launches (e.g. the
+    q/k/v | o | gate/up | down groups of a decoder block at some bit-widths)
+    driven end to end from HOST memory.
+
+    All distinct activation buffers of the step live in one contiguous device
+    block mirrored by one pinned host block, and all outputs likewise, so a
+    step is: one H2D copy of every input, the launches (replayed from a CUDA
+    graph after ``capture()``), one D2H copy of every output, one stream
+    synchronisation.  ``x_host`` / ``y_host`` are the pinned views the caller
+    fills / reads (one per distinct activation / per output, in plan order).
+    """
+
+    def __init__(self, plans):
+        torch = dev.require_cuda()
+        self.plans = list(plans)
+        xs, seen = [], {}
+        for p in self.plans:
+            for x in p.x:
+                if x.data_ptr() not in seen:
+                    seen[x.data_ptr()] = len(xs)
+                    xs.append(x)
+        ys = [y for p in self.plans for y in p.y]
+        n_x = sum(x.numel() for x in xs)
+        self._xd = torch.empty(n_x, dtype=torch.float16, device="cuda")
+        self._xh = torch.empty(n_x, dtype=torch.float16).pin_memory()
+        ybytes = sum(y.numel() * y.element_size() for y in ys)
+        self._yd = torch.empty(ybytes, dtype=torch.uint8, device="cuda")
+        self._yh = torch.empty(ybytes, dtype=torch.uint8).pin_memory()
+        # carve views, then rebind every plan onto them
+        xviews, xhost, off = [], [], 0
+        for x in xs:
+            n = x.numel()
+            xviews.append(self._xd[off:off + n].view(x.shape))
+            xhost.append(self._xh[off:off + n].view(x.shape))
+            off += n
+        yviews, yhost, off = [], [], 0
+        for y in ys:
+            nb = y.numel() * y.element_size()
+            yviews.append(self._yd[off:off + nb].view(y.dtype).view(y.shape))
+            yhost.append(self._yh[off:off + nb].view(y.dtype).view(y.shape))
+            off += nb
+        yi = 0
+        for p in self.plans:
+            p.rebind([xviews[seen[x.data_ptr()]] for x in p.x], yviews[yi:yi + len(p.y)])
+            yi += len(p.y)
+        self.x_host, self.y_host = xhost, yhost
+        self.h2d_bytes = n_x * 2
+        self.d2h_bytes = ybytes
+        self._graph = None
+
+    def launch(self):
+        for p in self.plans:
+            p.run()
+
+    def capture(self):
+        """Record the launches into a CUDA graph (run ``launch()`` once first)."""
+        torch = dev.require_cuda()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch()
+        self._graph = g
+        return g
+
+    def run_host(self):
+        """x_host -> device, the step's launches, device -> y_host; returns y_host."""
+        torch = dev.require_cuda()
+        self._xd.copy_(self._xh, non_blocking=True)
+        if self._graph is not None:
+            self._graph.replay()
+        else:
+            self.launch()
+        self._yh.copy_(self._yd, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.y_host

@@ -452,3 +452,33 @@ def test_large_shape_properties(api):
         rhs = float((a.double() * colsum).sum())
         scale = float((a.double().abs() * w.abs().sum(0)).sum())
         assert abs(lhs - rhs) <= 1e-5 * scale, (k, lhs, rhs)
+
+
+def test_step_plan_host_roundtrip(api):
+    # plan.StepPlan (one H2D of every activation, the launches from a graph, one
+    # D2H of every output) gives exactly the outputs of the single-layer API
+    import torch
+
+    from paper_2402_10517_b200 import plan
+
+    _, _, engine, _ = api
+    shapes = [(4096, 4096), (1100, 4096), (333, 3000)]
+    preps = [engine.prepare(_random_layer(api, 200 + i, r, c)) for i, (r, c) in enumerate(shapes)]
+    plans = [plan.GemvPlan(preps[:2], 3, grouped=True, pdl=True, shared_x=True),
+             plan.GemvPlan([preps[2]], 8, grouped=False, pdl=True)]
+    sp = plan.StepPlan(plans)
+    g = torch.Generator().manual_seed(5)
+    for x in sp.x_host:
+        x.copy_(torch.randn(x.shape, generator=g).half())
+    sp.launch()
+    torch.cuda.synchronize()
+    sp.capture()
+    y = [t.clone() for t in sp.run_host()]
+    assert not y[0].is_cuda and len(y) == 3
+    x0 = sp.x_host[0][0, :4096].clone()
+    x1 = sp.x_host[1][0, :3000].clone()
+    cfg3 = engine.GemvConfig(bit_width=3, activations_fp16=True)
+    cfg8 = engine.GemvConfig(bit_width=8, activations_fp16=True)
+    assert torch.equal(y[0][0], engine.gemv(preps[0], x0, cfg3))
+    assert torch.equal(y[1][0], engine.gemv(preps[1], x0, cfg3))
+    assert torch.equal(y[2][0], engine.gemv(preps[2], x1, cfg8))
