@@ -181,6 +181,26 @@ def time_graph(torch, fn, reps: int):
     return g, a.elapsed_time(b) / reps
 
 
+def measured_traffic():
+    """roofline.traffic: DRAM bytes (ncu dram__bytes_read.sum + write.sum) of the
+    GEMV launches captured by `ncu --set full` (tools/gpu_bench_profile.sh ->
+    profiles/r1_traffic.json: one k-group qkv | o | gate+up | down), scaled to
+    one step by their algorithmic bytes.  None when no capture is committed."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            tr = json.load(f)
+        dram = [l["dram_bytes"] for l in tr["launches"]]
+        if len(dram) != len(GROUPS):
+            return None, None
+        k = int(tr["launches"][0]["kernel"].split("<")[1].split(">")[0])
+        alg = [sum(alg_bytes(SHAPES[j][1], SHAPES[j][2], k) for j in grp) for grp in GROUPS]
+        ratio = sum(dram) / sum(alg)
+        return round(ratio * step_bytes()), {"dram_over_algorithmic": round(ratio, 4), "k": k,
+                                             "source": tr["source"]}
+    except Exception:
+        return None, None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -248,6 +268,7 @@ def run_ours(args):
     ms_per_step = ms / args.steps
     value = step_bytes() / (ms_per_step * 1e-3) / 1e9
     launches = len(plans) * args.steps
+    traffic, traffic_detail = measured_traffic()
 
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
@@ -262,9 +283,11 @@ def run_ours(args):
                    "l2": f"inputs > L2: weights rotated over {N_COPIES} copies (4 x 203 MB) per launch"},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": round(value, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(value / peak, 4), "peak_kind": peak_kind, "traffic": None,
+                     "frac": round(value / peak, 4), "peak_kind": peak_kind, "traffic": traffic,
+                     "traffic_detail": traffic_detail,
                      "note": "achieved = algorithmic bytes / CUDA-event time of the timed region "
-                             "(every launch in it is the GEMV kernel)"},
+                             "(every launch in it is the GEMV kernel); traffic = DRAM bytes per step "
+                             "estimated from the committed ncu capture"},
         "clocks": clocks,
     }
     if args.profile:

@@ -9,6 +9,6 @@ timeout 300 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TA
 timeout 300 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref_$TAG.json 2>> gpurun_out/bench_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
    python bench.py --profile --steps 2 --warmup 3 > /dev/null 2>> gpurun_out/bench_$TAG.err
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -s 80 -c 4 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv -s 80 -c 4 \
    -o gpurun_out/full_$TAG python bench.py --profile --steps 2 --warmup 3 > /dev/null 2>> gpurun_out/bench_$TAG.err
 tail -1 gpurun_out/pytest_$TAG.log; tail -3 gpurun_out/bench_$TAG.err

@@ -12,7 +12,7 @@ iN, iV = hdr.index("Kernel Name"), hdr.index("Metric Value")
 by = collections.defaultdict(list)
 for r in rows:
     name = r[iN]
-    short = "gemv_kernel" if "gemv_kernel" in name else name.split("(")[0][-70:]
+    short = "gemv_kernel" if "gemv" in name else name.split("(")[0][-70:]
     by[short].append(float(r[iV]))
 tot = sum(sum(v) for v in by.values())
 out.append(f"# {tag}: ncu launch list of `python bench.py --profile --steps 2 --warmup 3`\n")
@@ -54,6 +54,9 @@ want = [("Kernel Name", ""), ("gpu__time_duration.sum", "duration"), ("dram__byt
         ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
         ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts")]
 o2 = [f"# {tag}: `ncu --set full --clock-control none` of 4 GEMV launches inside the timed bench steps\n"]
+want += [("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe %"),
+         ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+         ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem conflicts")]
 o2.append("| " + " | ".join(n or "kernel" for _, n in want) + " |")
 o2.append("|" + "---|" * len(want))
 for d in data:
@@ -67,3 +70,16 @@ for d in data:
     o2.append("| " + " | ".join(vals) + " |")
 open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full.md"), "w").write("\n".join(o2) + "\n")
 print("\n".join(out[-8:])); print("\n".join(o2))
+
+# per-launch DRAM traffic vs algorithmic bytes (bench.py reads this for roofline.traffic)
+tr = []
+for d in data:
+    name = d[h.index("Kernel Name")]
+    if "gemv" not in name:
+        continue
+    rd = float(d[h.index("dram__bytes_read.sum")]); wr = float(d[h.index("dram__bytes_write.sum")])
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    rd *= scale.get(u[h.index("dram__bytes_read.sum")], 1); wr *= scale.get(u[h.index("dram__bytes_write.sum")], 1)
+    tr.append({"kernel": name.split("(")[0].replace("void ", ""), "dram_bytes": rd + wr})
+json.dump({"source": f"profiles/{tag}_ncu_full.md (ncu --set full)", "launches": tr},
+          open(os.path.join(ROOT, "profiles", f"{tag}_traffic.json"), "w"), indent=1)
