@@ -131,9 +131,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tW_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra W_%=;\n\t}" ::"r"(a),
-        "r"(parity)
+        "r"(parity), "r"(1000000)
         : "memory");
 }
 // try_wait with a suspend-time hint: a waiting warp sleeps in the barrier unit
@@ -511,7 +511,8 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
 #pragma unroll
     for (int i = 0; i < 8; ++i) xv[0][i] = xv[1][i] = 0u;
 
-    int pi = problem_of(L, first), pend = problem_end(L, pi), xb = 0, xph[2] = {0, 0};
+    int pi = problem_of(L, first), pend = problem_end(L, pi), xb = 0;
+    uint32_t xph = 0;  // bit b: phase parity of x buffer b
     int gs = grp;            // next ring stage of this warp group
     int item_gs = 0;         // first stage of the current item
     int slot = grp, ph = 0;  // ring slot / phase parity of stage gs (NST >= NG)
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
         const int xcol0 = 32 * su + 16 * cp + 4 * gset;
         const uint32_t xrow = saddr(xs + xb * L.xs_bytes) + (uint32_t)(gm < L.m_x ? gm : 0) * (uint32_t)(nt * 2048) +
                               (uint32_t)xcol0 * 2u;
-        const int64_t xcols = P.cols - xcol0;  // column limit relative to xrow
+        const int xcols = (int)P.cols - xcol0;  // column limit relative to xrow
         const int full_tiles = (int)(P.cols / kTileWeights);
         const uint32_t off = (uint32_t)(jl & 1) * 128u + (uint32_t)lane * 4u;
         float acc[2][4];
@@ -540,8 +541,8 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
 
         mbar_sleep(b_tready + 8 * (jl & 1), (jl >> 1) & 1);  // table of this item
         if (new_x) {  // activations of this layer staged
-            mbar_sleep(b_xfull + 8 * xb, xph[xb]);
-            xph[xb] ^= 1;
+            mbar_sleep(b_xfull + 8 * xb, (xph >> xb) & 1u);
+            xph ^= 1u << xb;
         }
 #pragma unroll 1
         for (; gs < item_gs + nt; gs += NG) {
@@ -565,7 +566,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
                     if (!xfull) {  // tail tile: columns >= cols are zero
 #pragma unroll
                         for (int p = 0; p < 4; ++p) {
-                            const int64_t c0 = (int64_t)tile * kTileWeights + 256 * p + 128 * j + 8 * wi;
+                            const int c0 = tile * kTileWeights + 256 * p + 128 * j + 8 * wi;
                             x8[2 * p] &= (c0 < xcols ? 0x0000FFFFu : 0u) | (c0 + 1 < xcols ? 0xFFFF0000u : 0u);
                             x8[2 * p + 1] &= (c0 + 2 < xcols ? 0x0000FFFFu : 0u) | (c0 + 3 < xcols ? 0xFFFF0000u : 0u);
                         }
