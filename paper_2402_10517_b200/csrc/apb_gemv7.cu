@@ -88,7 +88,7 @@ struct alignas(64) Launch7 {
     int64_t xs_bytes;  // one activation buffer
 };
 
-template <int K>
+template <int K, int NB = 1>
 struct Geo {
     static constexpr bool kPair = K <= 4;
     static constexpr int kEntries = kPair ? (1 << (2 * K)) : (1 << K);
@@ -102,11 +102,12 @@ struct Geo {
 #ifdef APB7_WC
     static constexpr int kWC = APB7_WC;
 #else
-    static constexpr int kWC = K == 8 ? 12 : 16;  // compute warps, groups of 4 (measured best per k)
+    // compute warps, groups of 4 (measured best per k; 8 for 4 batch pairs: registers)
+    static constexpr int kWC = NB >= 4 ? 8 : (K == 8 ? 12 : 16);
 #endif
     static constexpr int kNG = kWC / 4;
     static constexpr int kThreads = (kWC + 2) * 32;
-    static constexpr int kRedBytes = 2 * kWC * 2 * kRows * 4;  // [slot][warp][m][row] f32
+    static constexpr int kRedBytes = 2 * kWC * 2 * NB * kRows * 4;  // [slot][warp][m][row] f32
     // layout: tables | lut x2 | ring | xs x2 | red | barriers
     static constexpr int kLut = (kTableBytes + 1023) / 1024 * 1024;
     static constexpr int kRing = kLut + 2 * kLutSlot;
@@ -266,9 +267,12 @@ __device__ __forceinline__ void decode_word(const uint32_t* Q, uint32_t off, uin
     }
 }
 
-template <int K>
-__global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid_constant__ Launch7 L) {
-    using G = Geo<K>;
+// NB = batch pairs per launch (m_x <= 2 NB).  NB = 1 stages x in shared memory;
+// NB > 1 (small-batch GEMM, engine.py:312-341 with M <= 8) reads its B
+// fragments from global memory (L1 / L2 resident) so x never limits smem.
+template <int K, int NB>
+__global__ void __launch_bounds__(Geo<K, NB>::kThreads, 1) gemv7_kernel(const __grid_constant__ Launch7 L) {
+    using G = Geo<K, NB>;
     constexpr int WC = G::kWC, NG = G::kNG;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -409,25 +413,25 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
         };
         auto reduce = [&](int item, int pi, int slot) {
             const Prob7& P = L.prob[pi];
-            const int m_out = L.x_split ? 1 : L.m_x;
+            const int m_out = L.x_split ? (L.m_x >> 1) : L.m_x;
             const int64_t row0 = (int64_t)(item - P.item_begin) * kRows;
-            const float* r = red + slot * (WC * 2 * kRows);
+            const float* r = red + slot * (WC * 2 * NB * kRows);
             for (int i = lane; i < kRows * m_out; i += 32) {
                 const int rl = i & 15, m = i >> 4;
                 const int64_t row = row0 + rl;
                 if (row >= P.rows) continue;
                 float sum;
-                if (L.x_split) {
+                if (L.x_split) {  // batch rows (2m, 2m+1) = (hi, lo) halves of fp32 x
                     float hi = 0.f, lo = 0.f;
 #pragma unroll
-                    for (int w = 0; w < WC; ++w) hi += r[(w * 2 + 0) * kRows + rl];
+                    for (int w = 0; w < WC; ++w) hi += r[(w * 2 * NB + 2 * m) * kRows + rl];
 #pragma unroll
-                    for (int w = 0; w < WC; ++w) lo += r[(w * 2 + 1) * kRows + rl];
+                    for (int w = 0; w < WC; ++w) lo += r[(w * 2 * NB + 2 * m + 1) * kRows + rl];
                     sum = hi + lo;
                 } else {
                     sum = 0.f;
 #pragma unroll
-                    for (int w = 0; w < WC; ++w) sum += r[(w * 2 + m) * kRows + rl];
+                    for (int w = 0; w < WC; ++w) sum += r[(w * 2 * NB + m) * kRows + rl];
                 }
                 if (L.y_f16)
                     reinterpret_cast<__half*>(P.y)[(int64_t)m * P.ldy + row] = __float2half_rn(sum);
@@ -441,7 +445,7 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
         // activations of problem pi -> x buffer xb (one bulk copy per batch row;
         // columns past cols are masked by the compute warps)
         auto issue_x = [&](int pi, int xb) {
-            if (lane != 0) return;
+            if (NB > 1 || lane != 0) return;
             const Prob7& P = L.prob[pi];
             const uint32_t bytes = (uint32_t)((P.cols + 7) / 8 * 16);
             mbar_expect_tx(b_xfull + 8 * xb, bytes * L.m_x);
@@ -499,17 +503,22 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
     uint32_t plane_off[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) plane_off[j] = rho * 128 + (((su + 4 * j) ^ (rho & 7)) << 4) + cp * 8;
-    // B fragment role: column n = g; batch row gm = g >> 2, column set gset = (g >> 1) & 1.
-    // Live lanes read x[gm][tile*1024 + 256p + 8t + 4*gset .. +3] (8 bytes, raw
-    // layout: the 4 live addresses of a load are 8/32 B apart -> one wavefront);
-    // the others keep zeros.
-    const int gm = g >> 2, gset = (g >> 1) & 1;
-    const uint32_t xlive = (gm < L.m_x && (q >> 1) == (g & 1)) ? 1u : 0u;
-    const int xcol_lane = 32 * su + 4 * cp + 4 * gset;  // + tile*1024 + 256p + 128j + 8wi (+4cp via 2cp words)
-
-    uint32_t xv[2][8];
+    // B fragment role: column n = g; batch row gm = 2b + (g >> 2) for batch pair b,
+    // column set gset = (g >> 1) & 1.  Live lanes read x[gm][tile*1024 + 256p +
+    // 8t + 4*gset .. +3] (8 bytes; the 4 live addresses of a load are 8 / 32 B
+    // apart -> one wavefront); the others hold zeros (smem path) or read the
+    // all-zero array (global path).
+    const int gset = (g >> 1) & 1;
+    const bool xrole = (q >> 1) == (g & 1);
+    uint32_t xlive[NB];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) xv[0][i] = xv[1][i] = 0u;
+    for (int b = 0; b < NB; ++b) xlive[b] = (xrole && 2 * b + (g >> 2) < L.m_x) ? 1u : 0u;
+
+    uint32_t xv[NB][8];
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xv[b][i] = 0u;
 
     int pi = problem_of(L, first), pend = problem_end(L, pi), xb = 0;
     uint32_t xph = 0;  // bit b: phase parity of x buffer b
@@ -530,19 +539,33 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
         const int nt = P.n_tiles;
         // column of word t = 4ch + 2cp + wi: 8t = 32su + 128j + 16cp + 8wi
         const int xcol0 = 32 * su + 16 * cp + 4 * gset;
-        const uint32_t xrow = saddr(xs + xb * L.xs_bytes) + (uint32_t)(gm < L.m_x ? gm : 0) * (uint32_t)(nt * 2048) +
-                              (uint32_t)xcol0 * 2u;
-        const int xcols = (int)P.cols - xcol0;  // column limit relative to xrow
+        const int xcols = (int)P.cols - xcol0;  // column limit relative to the lane's x base
         const int full_tiles = (int)(P.cols / kTileWeights);
-        const uint32_t off = (uint32_t)(jl & 1) * 128u + (uint32_t)lane * 4u;
-        float acc[2][4];
+        uint32_t xrow_s = 0;                    // NB == 1: shared-memory x of this layer
+        const uint16_t* xrow_g[NB];             // NB > 1: global x rows
+        if constexpr (NB == 1) {
+            xrow_s = saddr(xs + xb * L.xs_bytes) + (uint32_t)((g >> 2) < L.m_x ? (g >> 2) : 0) * (uint32_t)(nt * 2048) +
+                     (uint32_t)xcol0 * 2u;
+        } else {
 #pragma unroll
-        for (int c2 = 0; c2 < 2; ++c2) acc[c2][0] = acc[c2][1] = acc[c2][2] = acc[c2][3] = 0.f;
+            for (int b = 0; b < NB; ++b)
+                xrow_g[b] = xlive[b] ? P.x + (int64_t)(2 * b + (g >> 2)) * P.ldx + xcol0 : g_zero_x;
+        }
+        const uint32_t off = (uint32_t)(jl & 1) * 128u + (uint32_t)lane * 4u;
+        float acc[NB][2][4];
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2) acc[b][c2][0] = acc[b][c2][1] = acc[b][c2][2] = acc[b][c2][3] = 0.f;
 
         mbar_sleep(b_tready + 8 * (jl & 1), (jl >> 1) & 1);  // table of this item
-        if (new_x) {  // activations of this layer staged
-            mbar_sleep(b_xfull + 8 * xb, (xph >> xb) & 1u);
-            xph ^= 1u << xb;
+        if (new_x) {
+            if constexpr (NB == 1) {  // activations of this layer staged
+                mbar_sleep(b_xfull + 8 * xb, (xph >> xb) & 1u);
+                xph ^= 1u << xb;
+            } else if (jl == 0) {
+                asm volatile("griddepcontrol.wait;" ::: "memory");  // x from the previous kernel
+            }
         }
 #pragma unroll 1
         for (; gs < item_gs + nt; gs += NG) {
@@ -550,7 +573,6 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
             mbar_sleep(b_full + 8 * slot, ph);
             if (warp == 0 && lane == 0 && gs == 0) APB_TL(3);
             const uint32_t sb = s_ring + slot * G::kStageBytes;
-            const uint32_t xa = xrow + (uint32_t)tile * 2048u;
             const bool xfull = tile < full_tiles;
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
@@ -559,16 +581,31 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
                 for (int p = 0; p < K; ++p) pv[K - 1 - p] = lds64(sb + p * 2048 + plane_off[j]);  // Q[i] = plane K-1-i
 #pragma unroll
                 for (int wi = 0; wi < 2; ++wi) {
-                    uint32_t(&x8)[8] = xv[wi];
-                    const uint32_t xo = (uint32_t)(256 * j + 16 * wi);  // bytes: 128j + 8wi columns
+                    const int cbase = tile * kTileWeights + 128 * j + 8 * wi;  // + 256p, relative to xcol0
 #pragma unroll
-                    for (int p = 0; p < 4; ++p) lds64_keep(x8[2 * p], x8[2 * p + 1], xa + xo + 512 * p, xlive);
-                    if (!xfull) {  // tail tile: columns >= cols are zero
+                    for (int b = 0; b < NB; ++b) {
+                        uint32_t(&x8)[8] = xv[b];
+                        if constexpr (NB == 1) {
+                            const uint32_t xa = xrow_s + (uint32_t)cbase * 2u;
 #pragma unroll
-                        for (int p = 0; p < 4; ++p) {
-                            const int c0 = tile * kTileWeights + 256 * p + 128 * j + 8 * wi;
-                            x8[2 * p] &= (c0 < xcols ? 0x0000FFFFu : 0u) | (c0 + 1 < xcols ? 0xFFFF0000u : 0u);
-                            x8[2 * p + 1] &= (c0 + 2 < xcols ? 0x0000FFFFu : 0u) | (c0 + 3 < xcols ? 0xFFFF0000u : 0u);
+                            for (int p = 0; p < 4; ++p) lds64_keep(x8[2 * p], x8[2 * p + 1], xa + 512 * p, xlive[0]);
+                        } else {
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) {
+                                const uint16_t* src = xrow_g[b] + cbase + 256 * p;
+                                if (!xfull && cbase + 256 * p >= xcols) src = g_zero_x;  // never read past ldx
+                                const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
+                                x8[2 * p] = v.x;
+                                x8[2 * p + 1] = v.y;
+                            }
+                        }
+                        if (!xfull) {  // tail tile: columns >= cols are zero
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) {
+                                const int c0 = cbase + 256 * p;
+                                x8[2 * p] &= (c0 < xcols ? 0x0000FFFFu : 0u) | (c0 + 1 < xcols ? 0xFFFF0000u : 0u);
+                                x8[2 * p + 1] &= (c0 + 2 < xcols ? 0x0000FFFFu : 0u) | (c0 + 3 < xcols ? 0xFFFF0000u : 0u);
+                            }
                         }
                     }
                     uint32_t Q[K];
@@ -585,22 +622,27 @@ __global__ void __launch_bounds__(Geo<K>::kThreads, 1) gemv7_kernel(const __grid
                         }
                     }
 #pragma unroll
-                    for (int p = 0; p < 4; ++p)
-                        mma16816(acc[p & 1], a[p * 4 + 0], a[p * 4 + 2], a[p * 4 + 1], a[p * 4 + 3], x8[2 * p],
-                                 x8[2 * p + 1]);
+                    for (int b = 0; b < NB; ++b)
+#pragma unroll
+                        for (int p = 0; p < 4; ++p)
+                            mma16816(acc[b][p & 1], a[p * 4 + 0], a[p * 4 + 2], a[p * 4 + 1], a[p * 4 + 3],
+                                     xv[b][2 * p], xv[b][2 * p + 1]);
                 }
             }
         }
         item_gs += nt;
-        // rows 2g / 2g+1 of batch row q>>1: D[g][2q'] + D[g+8][2q'+2] with q' = q & 2
-        float c[4];
+        // rows 2g / 2g+1 of batch row 2b + (q>>1): D[g][2q'] + D[g+8][2q'+2] with q' = q & 2
 #pragma unroll
-        for (int i = 0; i < 4; ++i) c[i] = acc[0][i] + acc[1][i];
-        const float o2 = __shfl_xor_sync(0xffffffffu, c[2], 1), o3 = __shfl_xor_sync(0xffffffffu, c[3], 1);
-        if ((q & 1) == 0) {
-            float* r = red + (jl & 1) * (WC * 2 * kRows) + (warp * 2 + (q >> 1)) * kRows + 2 * g;
-            r[0] = c[0] + o2;
-            r[1] = c[1] + o3;
+        for (int b = 0; b < NB; ++b) {
+            float c[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) c[i] = acc[b][0][i] + acc[b][1][i];
+            const float o2 = __shfl_xor_sync(0xffffffffu, c[2], 1), o3 = __shfl_xor_sync(0xffffffffu, c[3], 1);
+            if ((q & 1) == 0) {
+                float* r = red + (jl & 1) * (WC * 2 * NB * kRows) + (warp * 2 * NB + 2 * b + (q >> 1)) * kRows + 2 * g;
+                r[0] = c[0] + o2;
+                r[1] = c[1] + o3;
+            }
         }
         mbar_arrive(b_idone + 8 * (jl & 1));  // all lanes (release orders the partial stores)
         if (warp == 0 && lane == 0 && jl == 0) APB_TL(4);
@@ -665,15 +707,15 @@ static int sm_count() {
 constexpr size_t kSmemLimit = 227 * 1024;
 constexpr int kMaxStages = 16;
 
-template <int K>
+template <int K, int NB>
 static int launch(Launch7& L, int flags, cudaStream_t s) {
-    using G = Geo<K>;
+    using G = Geo<K, NB>;
     // ring depth: as many stages as fit (>= 3)
     int nst = kMaxStages;
     while (nst >= G::kNG && G::total(nst, L.xs_bytes) > kSmemLimit) --nst;
     if (nst < G::kNG || nst < 3) return -1;
     L.n_stages = nst;
-    auto kern = gemv7_kernel<K>;
+    auto kern = gemv7_kernel<K, NB>;
     static std::atomic<int> configured{0};
     if (!configured.load(std::memory_order_acquire)) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit) != cudaSuccess)
@@ -715,7 +757,9 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
         const char* e = std::getenv("APB_GEMV_V7");
         return e && e[0] == '0';
     }();
-    if (disabled || k < 3 || k > 8 || m_x > 2 || n > kMaxProb) return -1;
+    // batch rows <= 4 (measured: for 5..8 rows the 16-row mapping of apb_gemv.cu,
+    // which carries the batch in the MMA N dimension, is faster)
+    if (disabled || k < 3 || k > 8 || m_x > 4 || n > kMaxProb) return -1;
     for (int i = 0; i < n; ++i)
         if (padded[i] > kMaxCols) return -1;
     static thread_local Launch7 L;  // ~5 KB: kept off the stack
@@ -750,13 +794,19 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     L.total_cost = cost;
     L.xs_bytes = (int64_t)m_x * max_tiles * 2048;
     cudaStream_t s = (cudaStream_t)stream;
-    switch (k) {
-        case 3: return launch<3>(L, flags, s);
-        case 4: return launch<4>(L, flags, s);
-        case 5: return launch<5>(L, flags, s);
-        case 6: return launch<6>(L, flags, s);
-        case 7: return launch<7>(L, flags, s);
-        case 8: return launch<8>(L, flags, s);
+    const int nb = m_x <= 2 ? 1 : 2;
+    if (nb > 1) L.xs_bytes = 0;
+    switch (k * 8 + nb) {
+#define APB7_CASE(K)                                      \
+    case K * 8 + 1: return launch<K, 1>(L, flags, s);     \
+    case K * 8 + 2: return launch<K, 2>(L, flags, s);
+        APB7_CASE(3)
+        APB7_CASE(4)
+        APB7_CASE(5)
+        APB7_CASE(6)
+        APB7_CASE(7)
+        APB7_CASE(8)
+#undef APB7_CASE
     }
     return -1;
 }

@@ -33,6 +33,8 @@ __global__ void fill_half(__half* p, size_t n, uint32_t seed, float scale) {
 __global__ void ref_gemv(const uint8_t* planes, int64_t R, int64_t C, int64_t Cp, int k,
                          const __half* lut, const __half* x, double* y) {
     int64_t r = blockIdx.x;
+    x += blockIdx.y * ((C + 7) / 8 * 8);
+    y += blockIdx.y * R;
     double acc = 0;
     const int64_t rb = Cp / 8;
     for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
@@ -51,7 +53,7 @@ __global__ void ref_gemv(const uint8_t* planes, int64_t R, int64_t C, int64_t Cp
 
 struct Layer { int64_t R, C, Cp; std::vector<uint8_t*> planes; std::vector<__half*> lut; __half* x; float* y; };
 
-static Layer make_layer(int64_t R, int64_t C, int ncopy, uint32_t seed) {
+static Layer make_layer(int64_t R, int64_t C, int ncopy, uint32_t seed, int M) {
     Layer L; L.R = R; L.C = C; L.Cp = apb_pad_columns(C);
     size_t pb = (size_t)8 * R * (L.Cp / 8);
     for (int c = 0; c < ncopy; ++c) {
@@ -61,8 +63,8 @@ static Layer make_layer(int64_t R, int64_t C, int ncopy, uint32_t seed) {
         L.planes.push_back(p); L.lut.push_back(t);
     }
     int64_t ldx = (C + 7) / 8 * 8;
-    CK(cudaMalloc(&L.x, ldx * 2)); fill_half<<<64, 256>>>(L.x, ldx, seed + 5, 2.0f);
-    CK(cudaMalloc(&L.y, R * 4));
+    CK(cudaMalloc(&L.x, M * ldx * 2)); fill_half<<<64, 256>>>(L.x, M * ldx, seed + 5, 2.0f);
+    CK(cudaMalloc(&L.y, M * R * 4));
     return L;
 }
 
@@ -74,17 +76,18 @@ int main(int argc, char** argv) {
     std::string only = argc > 1 ? argv[1] : "";
     int konly = argc > 2 ? atoi(argv[2]) : 0;   // 0 = k 3..8
     if (argc > 3) reps = atoi(argv[3]);
+    const int M = argc > 4 ? atoi(argv[4]) : 1;  // batch rows
     CK(cudaSetDevice(0));
     cudaStream_t s; CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     struct Shape { const char* n; int64_t R, C; };
     std::vector<Shape> shapes = {{"4096x4096", 4096, 4096}, {"11008x4096", 11008, 4096}, {"4096x11008", 4096, 11008},
                                  {"28672x8192", 28672, 8192}};
-    double* yref; CK(cudaMalloc(&yref, 28672 * 8));
-    std::vector<double> h_ref(28672); std::vector<float> h_y(28672);
+    double* yref; CK(cudaMalloc(&yref, 8 * 28672 * 8));
+    std::vector<double> h_ref(8 * 28672); std::vector<float> h_y(8 * 28672);
     for (auto& sh : shapes) {
         if (!only.empty() && only.find(sh.n) == std::string::npos && only != "all") continue;
         int nc = sh.R * sh.C > 100000000 ? 2 : ncopy;
-        Layer L = make_layer(sh.R, sh.C, nc, 1234);
+        Layer L = make_layer(sh.R, sh.C, nc, 1234, M);
         CK(cudaDeviceSynchronize());
         printf("%-11s", sh.n);
         for (int k = 3; k <= 8; ++k) {
@@ -92,17 +95,17 @@ int main(int argc, char** argv) {
             int64_t ldx = (sh.C + 7) / 8 * 8;
             auto launch = [&](int c) {
                 int rc = apb_gemv(L.planes[c], 8, sh.R, sh.C, L.Cp, k, (const uint16_t*)(L.lut[c] + lut_off(sh.R, k)),
-                                  (const uint16_t*)L.x, 1, ldx, 0, L.y, APB_DTYPE_F32, sh.R, APB_FLAG_PDL, s);
+                                  (const uint16_t*)L.x, M, ldx, 0, L.y, APB_DTYPE_F32, sh.R, APB_FLAG_PDL, s);
                 if (rc) { fprintf(stderr, "apb_gemv rc=%d\n", rc); exit(1); }
             };
             // correctness vs naive reference (copy 0)
             launch(0); CK(cudaStreamSynchronize(s));
-            ref_gemv<<<sh.R, 256, 0, s>>>(L.planes[0], sh.R, sh.C, L.Cp, k, L.lut[0] + lut_off(sh.R, k), L.x, yref);
+            ref_gemv<<<dim3(sh.R, M), 256, 0, s>>>(L.planes[0], sh.R, sh.C, L.Cp, k, L.lut[0] + lut_off(sh.R, k), L.x, yref);
             CK(cudaStreamSynchronize(s));
-            CK(cudaMemcpy(h_y.data(), L.y, sh.R * 4, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(h_ref.data(), yref, sh.R * 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(h_y.data(), L.y, M * sh.R * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(h_ref.data(), yref, M * sh.R * 8, cudaMemcpyDeviceToHost));
             double num = 0, den = 0;
-            for (int64_t r = 0; r < sh.R; ++r) { num += (h_y[r] - h_ref[r]) * (h_y[r] - h_ref[r]); den += h_ref[r] * h_ref[r]; }
+            for (int64_t r = 0; r < M * sh.R; ++r) { num += (h_y[r] - h_ref[r]) * (h_y[r] - h_ref[r]); den += h_ref[r] * h_ref[r]; }
             double err = sqrt(num / den);
             // timing: graph of reps*nc launches
             cudaGraph_t g; cudaGraphExec_t ge;
@@ -117,7 +120,7 @@ int main(int argc, char** argv) {
                 float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
             }
             double us = best * 1e3 / (reps * nc);
-            double bytes = (double)sh.R * sh.C * k / 8 + sh.R * (1 << k) * 2 + sh.C * 2 + sh.R * 2;
+            double bytes = (double)sh.R * sh.C * k / 8 + sh.R * (1 << k) * 2 + M * (sh.C * 2 + sh.R * 2);
             printf(" | k%d %6.2fus %5.0fGB/s%s", k, us, bytes / us * 1e-3, err < 1e-3 ? "" : " ERR");
             if (err >= 1e-3) printf("(%.2e)", err);
             fflush(stdout);
