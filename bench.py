@@ -297,6 +297,8 @@ def run_ours(args):
     if world == 1:
         result["per_gemv_us"] = per_gemv_detail(torch, plan, copies)
         result["grouped_all7_GBps"] = grouped_all7(torch, plan, copies)
+        if not args.no_decode:
+            result["decode_step"] = run_decode(torch)
     if rank == 0:
         if world == 1:
             result["e2e"] = run_e2e_step(torch, plans, world)
@@ -308,6 +310,52 @@ def run_ours(args):
         print(json.dumps(result))
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_decode(torch, steps: int = 20):
+    """BASELINE config C5: full random-init Llama-2-7B single-token decode step
+    (32 blocks, every linear through the bitplane GEMV at bit-width k, torch glue,
+    one CUDA graph per k, context 1024) -> tokens/s; plus GPU packer throughput
+    (pack_bitplanes + permute_layout of an 11008x4096 code matrix, 8 planes)."""
+    from paper_2402_10517_b200 import bitplane
+    from paper_2402_10517_b200.decode import DecodeModel
+
+    model = DecodeModel(context=1024)
+    out = {"model": "llama-2-7b shapes, 32 blocks, random-init", "context": 1024, "batch": 1,
+           "glue": "fused sm_100a kernels (residual+RMSNorm, RoPE+KV append, SiLU*up) + torch SDPA "
+                   "attention + cuBLAS fp16 LM head", "per_k": {}}
+    for k in BITS:
+        model.capture(k)
+        for _ in range(3):
+            model.step(k)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            model.step(k)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        out["per_k"][f"k{k}"] = {"ms_per_token": round(ms, 3), "tokens_per_s": round(1e3 / ms, 1),
+                                 "quantized_GBps": round(model.quantized_bytes(k) / (ms * 1e-3) / 1e9, 1)}
+    del model
+    torch.cuda.empty_cache()
+    # packer
+    g = torch.Generator(device="cuda").manual_seed(7)
+    codes = torch.randint(0, 256, (11008, 4096), dtype=torch.uint8, device="cuda", generator=g)
+    t = bitplane.pack_bitplanes(codes, 8)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(20):
+        t = bitplane.pack_bitplanes(codes, 8)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / 20
+    nbytes = codes.numel() + t.planes.numel()
+    out["packer"] = {"shape": "11008x4096 codes -> 8 bitplanes (linear layout)", "ms": round(ms, 4),
+                     "GBps": round(nbytes / (ms * 1e-3) / 1e9, 1)}
+    return out
 
 
 def per_gemv_detail(torch, plan, copies):
@@ -467,6 +515,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--profile", action="store_true",
                     help="profiling run (under ncu): eager launches, skip detail/e2e/CPU legs")
+    ap.add_argument("--no-decode", action="store_true", help="skip the C5 decode-step leg")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

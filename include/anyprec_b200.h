@@ -123,6 +123,20 @@ int apb_dequant(const uint8_t* planes, int n_max, int64_t rows, int64_t cols,
 int apb_split_x(const float* x, int m, int64_t cols, int64_t ldx_in, uint16_t* out,
                 int64_t ldx_out, int round_only, void* stream);
 
+/* Fused glue of a decoder block around the GEMVs (decode-step measurement,
+ * BASELINE config C5; outside the reference's hot path).  Device pointers,
+ * fp16 = uint16 bit patterns, one token wide.
+ *   apb_rms_residual: resid (f32) += add (f16, may be NULL); out = rmsnorm(resid) * w
+ *   apb_rope_cache  : q_out = rope(q); k_cache[h][.] = rope(k); v_cache[h][.] = v
+ *                     (cache pointers at the new position, head stride in elements)
+ *   apb_silu_mul    : out = silu(gate) * up */
+int apb_rms_residual(float* resid, const uint16_t* add, const uint16_t* w, uint16_t* out, int64_t n, float eps,
+                     void* stream);
+int apb_rope_cache(const uint16_t* q, const uint16_t* k, const uint16_t* v, const float* cosv, const float* sinv,
+                   uint16_t* q_out, uint16_t* k_cache, uint16_t* v_cache, int heads, int head_dim,
+                   int64_t cache_head_stride, void* stream);
+int apb_silu_mul(const uint16_t* gate, const uint16_t* up, uint16_t* out, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,164 @@
+"""Single-token decode step of a Llama-2-style decoder with any-precision
+quantized linears (BASELINE config C5).
+
+Every linear of every decoder block (q/k/v/o, gate/up/down; arch.py:74-81 of
+the reference lists the same seven per block) is one n_max-bit bitplane parent
+served at a per-step bit-width k through the B200 GEMV (plan.GemvPlan, grouped
+q/k/v and gate/up launches, fp16 outputs, PDL chain).  The glue around them is
+three fused sm_100a kernels of csrc/apb_decode.cu (residual add + RMSNorm
+writing the next GEMV's activation buffer, RoPE + KV-cache append, SiLU*up) plus
+PyTorch's SDPA for attention over the cache and a cuBLAS fp16 LM head; the
+whole step is captured in one CUDA graph per k.  Weights are random-init (codes uniform in [0, 2^n_max),
+sorted N(0,1) centroid rows, helpers.random_layer semantics), activations are
+real (embedding lookup of a token id, norms with unit weights).
+
+This is a measurement vehicle for the quantized hot path inside a full decode
+step, not a model loader: there is no tokenizer, no checkpoint, no sampling
+beyond argmax.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import _device as dev
+from .layer import AnyPrecisionLayer
+
+
+@dataclass
+class LlamaConfig:
+    hidden: int = 4096
+    intermediate: int = 11008
+    heads: int = 32
+    layers: int = 32
+    vocab: int = 32000
+    rope_theta: float = 10000.0
+    n_min: int = 3
+    n_max: int = 8
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.heads
+
+
+def _random_prepared(torch, engine, rows, cols, cfg, g):
+    codes = torch.randint(0, 1 << cfg.n_max, (rows, cols), dtype=torch.uint8, device="cuda", generator=g)
+    tables = {k: torch.sort(torch.randn(rows, 1 << k, device="cuda", generator=g), dim=1).values.half() * 0.02
+              for k in range(cfg.n_min, cfg.n_max + 1)}
+    layer = AnyPrecisionLayer(n_min=cfg.n_min, n_max=cfg.n_max, codes=codes, centroid_tables=tables,
+                              shape=(rows, cols))
+    prep = engine.prepare(layer)
+    del codes
+    return prep
+
+
+class DecodeModel:
+    """Random-init quantized decoder; ``step(k)`` decodes one token at bit-width k."""
+
+    def __init__(self, cfg: LlamaConfig = LlamaConfig(), context: int = 1024, seed: int = 0):
+        torch = dev.require_cuda()
+        from . import engine, plan
+
+        self.cfg, self.context = cfg, context
+        H, I, nh, hd = cfg.hidden, cfg.intermediate, cfg.heads, cfg.head_dim
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        self.blocks = []
+        for _ in range(cfg.layers):
+            names = [("q", H, H), ("k", H, H), ("v", H, H), ("o", H, H), ("gate", I, H), ("up", I, H),
+                     ("down", H, I)]
+            self.blocks.append({n: _random_prepared(torch, engine, r, c, cfg, g) for n, r, c in names})
+        self.embed = (torch.randn(cfg.vocab, H, device="cuda", generator=g) * 0.02).half()
+        self.lm_head = (torch.randn(cfg.vocab, H, device="cuda", generator=g) * 0.02).half()
+        self.norm_w = torch.ones(H, device="cuda", dtype=torch.float16)
+        # KV cache filled with `context` random past positions; the new token is position `context`
+        self.k_cache = [torch.randn(1, nh, context + 1, hd, device="cuda", generator=g).half()
+                        for _ in range(cfg.layers)]
+        self.v_cache = [torch.randn(1, nh, context + 1, hd, device="cuda", generator=g).half()
+                        for _ in range(cfg.layers)]
+        inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, device="cuda").float() / hd))
+        ang = float(context) * inv
+        self.cos, self.sin = torch.cos(ang).contiguous(), torch.sin(ang).contiguous()
+        self.resid = torch.zeros(H, device="cuda", dtype=torch.float32)
+        self.qbuf = torch.zeros(nh * hd, device="cuda", dtype=torch.float16)
+        self.hbuf = torch.zeros(1, H, device="cuda", dtype=torch.float16)
+        self.token = torch.zeros(1, dtype=torch.long, device="cuda")
+        self.next_token = torch.zeros(1, dtype=torch.long, device="cuda")
+        self._plans, self._graphs = {}, {}
+        self._plan_mod = plan
+
+    # ---- per-k launch plans: x / y buffers shared by every block -----------------
+    def _plans_for(self, k: int):
+        if k in self._plans:
+            return self._plans[k]
+        plan = self._plan_mod
+        per_block = []
+        for blk in self.blocks:
+            qkv = plan.GemvPlan([blk["q"], blk["k"], blk["v"]], k, grouped=True, pdl=True, shared_x=True,
+                                y_fp16=True)
+            o = plan.GemvPlan([blk["o"]], k, grouped=True, pdl=True, y_fp16=True)
+            gu = plan.GemvPlan([blk["gate"], blk["up"]], k, grouped=True, pdl=True, shared_x=True,
+                               y_fp16=True)
+            dn = plan.GemvPlan([blk["down"]], k, grouped=True, pdl=True, y_fp16=True)
+            per_block.append((qkv, o, gu, dn))
+        self._plans[k] = per_block
+        return per_block
+
+    def _forward(self, k: int):
+        torch = dev.require_cuda()
+        from ._lib import check, load
+
+        lib, st = load(), dev.stream_ptr()
+        cfg, ctx = self.cfg, self.context
+        nh, hd, H, I = cfg.heads, cfg.head_dim, cfg.hidden, cfg.intermediate
+        P = dev.ptr
+        self.resid.copy_(self.embed[self.token].view(H).float())
+        add = None
+        for li, (qkv, o, gu, dn) in enumerate(self._plans_for(k)):
+            check(lib.apb_rms_residual(P(self.resid), add, P(self.norm_w), P(qkv.x[0]), H, 1e-5, st),
+                  "apb_rms_residual")
+            qkv.run()
+            kc, vc = self.k_cache[li], self.v_cache[li]
+            check(lib.apb_rope_cache(P(qkv.y[0]), P(qkv.y[1]), P(qkv.y[2]), P(self.cos), P(self.sin),
+                                     P(self.qbuf), P(kc) + ctx * hd * 2, P(vc) + ctx * hd * 2, nh, hd,
+                                     (ctx + 1) * hd, st), "apb_rope_cache")
+            att = torch.nn.functional.scaled_dot_product_attention(self.qbuf.view(1, nh, 1, hd), kc, vc)
+            o.x[0][:, :H].copy_(att.view(1, H))
+            o.run()
+            check(lib.apb_rms_residual(P(self.resid), P(o.y[0]), P(self.norm_w), P(gu.x[0]), H, 1e-5, st),
+                  "apb_rms_residual")
+            gu.run()
+            check(lib.apb_silu_mul(P(gu.y[0]), P(gu.y[1]), P(dn.x[0]), I, st), "apb_silu_mul")
+            dn.run()
+            add = P(dn.y[0])
+        check(lib.apb_rms_residual(P(self.resid), add, P(self.norm_w), P(self.hbuf), H, 1e-5, st),
+              "apb_rms_residual")
+        logits = self.hbuf @ self.lm_head.t()
+        self.next_token.copy_(torch.argmax(logits, dim=-1))
+
+    def capture(self, k: int):
+        torch = dev.require_cuda()
+        self._forward(k)  # warm-up: plans, kernel attributes, library workspaces
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            self._forward(k)
+        self._graphs[k] = gr
+        return gr
+
+    def step(self, k: int):
+        """Decode one token at bit-width k (graph replay once captured)."""
+        gr = self._graphs.get(k)
+        if gr is None:
+            self._forward(k)
+        else:
+            gr.replay()
+        return self.next_token
+
+    def quantized_bytes(self, k: int) -> int:
+        """Algorithmic bytes the quantized linears read per token."""
+        tot = 0
+        for blk in self.blocks:
+            for p in blk.values():
+                r, c = p.tensor.rows, p.tensor.cols
+                tot += r * c * k // 8 + r * (1 << k) * 2 + c * 2 + r * 2
+        return tot
