@@ -54,13 +54,16 @@ constexpr int kMaxCols = 64 * 1024;  // padded columns per layer on this path
 __device__ __align__(16) uint16_t g_zero_x[kMaxCols];
 
 #ifdef APB_TIMELINE
-// Debug builds (tools/kbench timeline): per-CTA globaltimer stamps (ns).
-__device__ unsigned long long g_tl7[1024 * 8];
-__device__ __forceinline__ void tl_stamp(int i) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_tl7[blockIdx.x * 8 + i] = t;
-}
+// Debug builds (tools/kbench timeline / chain): per-launch, per-CTA globaltimer
+// stamps (ns) at [launch % 64][block][8]; the launch index is a host-side
+// counter carried in Launch7::tl_launch.
+__device__ unsigned long long g_tl7[64 * 512 * 8];
+#define tl_stamp(i)                                                                              \
+    do {                                                                                         \
+        unsigned long long t_;                                                                   \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
+        g_tl7[((size_t)(L.tl_launch % 64) * 512 + blockIdx.x) * 8 + (i)] = t_;                  \
+    } while (0)
 #define APB_TL(i) tl_stamp(i)
 #else
 #define APB_TL(i) \
@@ -86,6 +89,7 @@ struct alignas(64) Launch7 {
     int m_x, x_split, y_f16;
     int n_stages;      // ring depth
     int64_t xs_bytes;  // one activation buffer
+    int tl_launch;     // APB_TIMELINE builds: launch index
 };
 
 template <int K, int NB = 1>
@@ -743,9 +747,11 @@ static int launch(Launch7& L, int flags, cudaStream_t s) {
 // Called by apb_gemv_grouped (apb_gemv.cu) after argument validation.
 // Returns -1 when this kernel does not apply (caller falls back), else a status.
 #ifdef APB_TIMELINE
+static int g_tl_host_launch = 0;
 extern "C" int apb7_read_timeline(unsigned long long* host, int n) {
-    return cudaMemcpyFromSymbol(host, apb7::g_tl7, sizeof(unsigned long long) * 8 * n) == cudaSuccess ? 0 : 5;
+    return cudaMemcpyFromSymbol(host, apb7::g_tl7, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 5;
 }
+extern "C" void apb7_timeline_reset(void) { g_tl_host_launch = 0; }
 #endif
 
 extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
@@ -793,6 +799,9 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     L.n_items = items;
     L.total_cost = cost;
     L.xs_bytes = (int64_t)m_x * max_tiles * 2048;
+#ifdef APB_TIMELINE
+    L.tl_launch = g_tl_host_launch++;
+#endif
     cudaStream_t s = (cudaStream_t)stream;
     const int nb = m_x <= 2 ? 1 : 2;
     if (nb > 1) L.xs_bytes = 0;

@@ -28,8 +28,14 @@ int main() {
             apb_gemv(planes, 8, R, C, Cp, k, lut, x, 1, C, 0, y, APB_DTYPE_F32, R, 0, s);
             cudaEventRecord(b, s); CK(cudaStreamSynchronize(s));
             float ms; cudaEventElapsedTime(&ms, a, b);
-            std::vector<unsigned long long> t(148 * 8);
-            apb7_read_timeline(t.data(), 148);
+            std::vector<unsigned long long> t(64 * 512 * 8);
+            apb7_read_timeline(t.data(), 64 * 512 * 8);
+            { // the timed launch is the newest: find the launch slot with the latest start
+                int best = 0; unsigned long long bt = 0;
+                for (int l = 0; l < 64; ++l) if (t[(size_t)l * 512 * 8] > bt) { bt = t[(size_t)l * 512 * 8]; best = l; }
+                std::vector<unsigned long long> u(t.begin() + (size_t)best * 512 * 8, t.begin() + (size_t)(best + 1) * 512 * 8);
+                t.swap(u);
+            }
             unsigned long long t0 = ~0ull, tend = 0;
             for (int c = 0; c < 148; ++c) if (t[c * 8]) { t0 = std::min(t0, t[c * 8]); tend = std::max(tend, t[c * 8 + 5]); }
             printf("%lldx%lld k=%d event %.2f us, CTA span %.2f us\n", (long long)R, (long long)C, k, ms * 1e3, (tend - t0) / 1e3);
