@@ -92,7 +92,7 @@ struct alignas(64) Launch7 {
     int tl_launch;     // APB_TIMELINE builds: launch index
 };
 
-template <int K, int NB = 1>
+template <int K, int NB = 1, int CPS = 1>
 struct Geo {
     static constexpr bool kPair = K <= 4;
     static constexpr int kEntries = kPair ? (1 << (2 * K)) : (1 << K);
@@ -106,8 +106,9 @@ struct Geo {
 #ifdef APB7_WC
     static constexpr int kWC = APB7_WC;
 #else
-    // compute warps, groups of 4 (measured best per k; 8 for 4 batch pairs: registers)
-    static constexpr int kWC = NB >= 4 ? 8 : (K == 8 ? 12 : 16);
+    // compute warps, groups of 4 (measured best per k; 8 for 4 batch pairs: registers;
+    // 8 when two CTAs share an SM)
+    static constexpr int kWC = (NB >= 4 || CPS == 2) ? 8 : (K == 8 ? 12 : 16);
 #endif
     static constexpr int kNG = kWC / 4;
     static constexpr int kThreads = (kWC + 2) * 32;
@@ -274,9 +275,9 @@ __device__ __forceinline__ void decode_word(const uint32_t* Q, uint32_t off, uin
 // NB = batch pairs per launch (m_x <= 2 NB).  NB = 1 stages x in shared memory;
 // NB > 1 (small-batch GEMM, engine.py:312-341 with M <= 8) reads its B
 // fragments from global memory (L1 / L2 resident) so x never limits smem.
-template <int K, int NB>
-__global__ void __launch_bounds__(Geo<K, NB>::kThreads, 1) gemv7_kernel(const __grid_constant__ Launch7 L) {
-    using G = Geo<K, NB>;
+template <int K, int NB, int CPS>
+__global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(const __grid_constant__ Launch7 L) {
+    using G = Geo<K, NB, CPS>;
     constexpr int WC = G::kWC, NG = G::kNG;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -313,6 +314,17 @@ __global__ void __launch_bounds__(Geo<K, NB>::kThreads, 1) gemv7_kernel(const __
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+
+    // activations of problem pi -> x buffer xb (one bulk copy per batch row;
+    // columns past cols are masked by the compute warps).  One thread.
+    auto issue_x_one = [&](int pi, int xb) {
+        const Prob7& P = L.prob[pi];
+        const uint32_t bytes = (uint32_t)((P.cols + 7) / 8 * 16);
+        mbar_expect_tx(b_xfull + 8 * xb, bytes * L.m_x);
+        for (int m = 0; m < L.m_x; ++m)
+            bulk_g2s(saddr(xs + xb * L.xs_bytes) + m * P.n_tiles * 2048, P.x + (int64_t)m * P.ldx, bytes,
+                     b_xfull + 8 * xb);
+    };
 
     if (warp == WC) {
         // ============================ producer (TMA) ============================
@@ -450,27 +462,24 @@ __global__ void __launch_bounds__(Geo<K, NB>::kThreads, 1) gemv7_kernel(const __
         // columns past cols are masked by the compute warps)
         auto issue_x = [&](int pi, int xb) {
             if (NB > 1 || lane != 0) return;
-            const Prob7& P = L.prob[pi];
-            const uint32_t bytes = (uint32_t)((P.cols + 7) / 8 * 16);
-            mbar_expect_tx(b_xfull + 8 * xb, bytes * L.m_x);
-            for (int m = 0; m < L.m_x; ++m)
-                bulk_g2s(saddr(xs + xb * L.xs_bytes) + m * P.n_tiles * 2048, P.x + (int64_t)m * P.ldx, bytes,
-                         b_xfull + 8 * xb);
+            issue_x_one(pi, xb);
         };
         // tables depend only on the weights: they are built before the previous
         // kernel of the stream has finished (PDL); x is read and y written after
         int pi = problem_of(L, first), pend = problem_end(L, pi), xb = 0;
         int pi_hist[2] = {pi, pi};
-        // x of the first layer: its bulk copy overlaps the centroid-row / plane
-        // latency of the first item.  (A CTA of this kernel only becomes resident
-        // once the previous kernel's CTAs leave the SM, so the PDL wait is short.)
-        asm volatile("griddepcontrol.wait;" ::: "memory");  // x / y of earlier kernels
-        issue_x(pi, 0);
-        if (lane == 0) APB_TL(2);
+        // The first layer's x is issued by compute warp 0 (after its PDL wait), so
+        // the first tables -- weights only -- are built even while the previous
+        // kernel of the stream is still running.
+        bool waited = false;
 #pragma unroll 1
         for (int jl = 0; jl < n_local + 2; ++jl) {
             if (jl >= 2) {  // item jl-2 done by every compute warp: reduce it, free its slot
                 mbar_wait(b_idone + 8 * (jl & 1), ((jl - 2) >> 1) & 1);
+                if (!waited) {  // y of earlier kernels (PDL); compute warp 0 already waited
+                    asm volatile("griddepcontrol.wait;" ::: "memory");
+                    waited = true;
+                }
                 reduce(first + jl - 2, pi_hist[jl & 1], jl & 1);
             }
             if (jl < n_local) {
@@ -479,6 +488,10 @@ __global__ void __launch_bounds__(Geo<K, NB>::kThreads, 1) gemv7_kernel(const __
                     pi = problem_of(L, item);
                     pend = problem_end(L, pi);
                     xb ^= 1;
+                    if (!waited) {
+                        asm volatile("griddepcontrol.wait;" ::: "memory");
+                        waited = true;
+                    }
                     issue_x(pi, xb);
                 }
                 pi_hist[jl & 1] = pi;
@@ -565,6 +578,13 @@ __global__ void __launch_bounds__(Geo<K, NB>::kThreads, 1) gemv7_kernel(const __
         mbar_sleep(b_tready + 8 * (jl & 1), (jl >> 1) & 1);  // table of this item
         if (new_x) {
             if constexpr (NB == 1) {  // activations of this layer staged
+                if (jl == 0 && warp == 0) {  // first layer: x / y of earlier kernels (PDL), then x
+                    asm volatile("griddepcontrol.wait;" ::: "memory");
+                    if (lane == 0) {
+                        issue_x_one(pi, 0);
+                        APB_TL(2);
+                    }
+                }
                 mbar_sleep(b_xfull + 8 * xb, (xph >> xb) & 1u);
                 xph ^= 1u << xb;
             } else if (jl == 0) {
@@ -709,24 +729,46 @@ static int sm_count() {
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
+constexpr size_t kSmemLimit2 = 113 * 1024;  // per CTA with two CTAs per SM
 constexpr int kMaxStages = 16;
 
+// Two CTAs per SM when an 8-compute-warp CTA with >= 4 ring stages fits in half
+// the shared memory: a CTA that finishes early frees half an SM for the next
+// kernel of a PDL chain while its neighbour still works, and the work
+// granularity halves.  APB7_CPS=1|2 forces the choice (tuning).
 template <int K, int NB>
+static int choose_cps(const Launch7& L) {
+    static const int forced = [] {
+        const char* e = std::getenv("APB7_CPS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced == 1) return 1;
+    const bool fits2 = NB == 1 && Geo<K, NB, 2>::total(4, L.xs_bytes) <= kSmemLimit2;
+    if (forced == 2) return fits2 ? 2 : 1;
+    // measured (tools/kbench): a win at k = 3 for every shape; at larger k only
+    // for short launches (<= 2.5 items per SM), where cross-kernel overlap and
+    // granularity dominate -- on long launches the 8-warp CTAs lose ~4 %.
+    const bool short_launch = 2 * L.n_items <= 5 * sm_count();
+    return fits2 && (K == 3 || short_launch) ? 2 : 1;
+}
+
+template <int K, int NB, int CPS>
 static int launch(Launch7& L, int flags, cudaStream_t s) {
-    using G = Geo<K, NB>;
+    using G = Geo<K, NB, CPS>;
+    const size_t limit = CPS == 2 ? kSmemLimit2 : kSmemLimit;
     // ring depth: as many stages as fit (>= 3)
     int nst = kMaxStages;
-    while (nst >= G::kNG && G::total(nst, L.xs_bytes) > kSmemLimit) --nst;
+    while (nst >= G::kNG && G::total(nst, L.xs_bytes) > limit) --nst;
     if (nst < G::kNG || nst < 3) return -1;
     L.n_stages = nst;
-    auto kern = gemv7_kernel<K, NB>;
+    auto kern = gemv7_kernel<K, NB, CPS>;
     static std::atomic<int> configured{0};
     if (!configured.load(std::memory_order_acquire)) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit) != cudaSuccess)
             return APB_ERR_CUDA;
         configured.store(1, std::memory_order_release);
     }
-    int grid = sm_count();
+    int grid = CPS * sm_count();
     if (grid > L.n_items) grid = L.n_items;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -806,9 +848,10 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     const int nb = m_x <= 2 ? 1 : 2;
     if (nb > 1) L.xs_bytes = 0;
     switch (k * 8 + nb) {
-#define APB7_CASE(K)                                      \
-    case K * 8 + 1: return launch<K, 1>(L, flags, s);     \
-    case K * 8 + 2: return launch<K, 2>(L, flags, s);
+#define APB7_CASE(K)                                                                                  \
+    case K * 8 + 1:                                                                                   \
+        return choose_cps<K, 1>(L) == 2 ? launch<K, 1, 2>(L, flags, s) : launch<K, 1, 1>(L, flags, s); \
+    case K * 8 + 2: return launch<K, 2, 1>(L, flags, s);
         APB7_CASE(3)
         APB7_CASE(4)
         APB7_CASE(5)
