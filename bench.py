@@ -297,6 +297,8 @@ def run_ours(args):
     if world == 1:
         result["per_gemv_us"] = per_gemv_detail(torch, plan, copies)
         result["grouped_all7_GBps"] = grouped_all7(torch, plan, copies)
+        result["small_batch_C3"] = small_batch_detail(torch, plan, copies)
+        result["shard70b_C4_per_rank"] = shard70b_detail(torch, plan)
         if not args.no_decode:
             result["decode_step"] = run_decode(torch)
     if rank == 0:
@@ -355,6 +357,67 @@ def run_decode(torch, steps: int = 20):
     nbytes = codes.numel() + t.planes.numel()
     out["packer"] = {"shape": "11008x4096 codes -> 8 bitplanes (linear layout)", "ms": round(ms, 4),
                      "GBps": round(nbytes / (ms * 1e-3) / 1e9, 1)}
+    return out
+
+
+def _chain_us(torch, plan, preps_copies, k, m, reps=10):
+    """µs per launch of a PDL chain of 5 x len(copies) launches (rotating copies)."""
+    ps = [plan.GemvPlan([c], k, m=m, grouped=False, pdl=True) for c in preps_copies]
+    for p in ps:
+        for x in p.x:
+            x.normal_()
+
+    def chain():
+        for _ in range(5):
+            for p in ps:
+                p.run()
+
+    _, ms = time_graph(torch, chain, reps)
+    return ms * 1e3 / (5 * len(ps))
+
+
+def small_batch_detail(torch, plan, copies):
+    """BASELINE config C3: any-precision GEMM at batch M = 1, 2, 4, 8 on the
+    Llama-2-7B MLP shapes (gate/up 11008x4096, down 4096x11008) at k = 3, 4, 8
+    (fp16 activations, each decoded weight reused across the batch)."""
+    out = {}
+    for li, name in ((4, "gate_11008x4096"), (6, "down_4096x11008")):
+        r, c = SHAPES[li][1], SHAPES[li][2]
+        for k in (3, 4, 8):
+            for m in (1, 2, 4, 8):
+                us = _chain_us(torch, plan, [cp[li] for cp in copies], k, m)
+                out.setdefault(name, {}).setdefault(f"k{k}", {})[f"M{m}"] = {
+                    "us": round(us, 2), "GBps": round(alg_bytes(r, c, k, m) / (us * 1e-6) / 1e9, 1)}
+    return out
+
+
+def shard70b_detail(torch, plan):
+    """BASELINE config C4 on one GPU: the per-rank GEMV of the Llama-2-70B layer
+    shapes row-sharded over P = 1, 2, 4, 8 ranks (each rank owns a contiguous
+    R/P-row slab; k = 3, 4, 8).  The NCCL all-gather of the y slices that follows
+    on a multi-GPU box is not part of this single-GPU number."""
+    from paper_2402_10517_b200 import AnyPrecisionLayer, engine
+
+    shapes = [("8192x8192", 8192, 8192), ("28672x8192", 28672, 8192), ("8192x28672", 8192, 28672)]
+    out = {}
+    g = torch.Generator(device="cuda").manual_seed(70)
+    for name, rows, cols in shapes:
+        for P in (1, 2, 4, 8):
+            r = rows // P
+            copies = []
+            for _ in range(2):
+                codes = torch.randint(0, 256, (r, cols), dtype=torch.uint8, device="cuda", generator=g)
+                tables = {k: torch.sort(torch.randn(r, 1 << k, device="cuda", generator=g), 1).values.half()
+                          for k in range(3, 9)}
+                copies.append(engine.prepare(AnyPrecisionLayer(n_min=3, n_max=8, codes=codes,
+                                                               centroid_tables=tables, shape=(r, cols))))
+                del codes
+            for k in (3, 4, 8):
+                us = _chain_us(torch, plan, copies, k, 1, reps=5)
+                out.setdefault(name, {}).setdefault(f"P{P}", {})[f"k{k}"] = {
+                    "rank_rows": r, "us": round(us, 2),
+                    "GBps": round(alg_bytes(r, cols, k) / (us * 1e-6) / 1e9, 1)}
+            del copies
     return out
 
 

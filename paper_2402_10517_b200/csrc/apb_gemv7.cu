@@ -78,6 +78,7 @@ struct Prob7 {
     int n_tiles;
     int item_begin;
     int64_t cost_begin;
+    int xid;  // problems with equal xid read the same activations (staged once)
 };
 
 struct alignas(64) Launch7 {
@@ -89,6 +90,7 @@ struct alignas(64) Launch7 {
     int m_x, x_split, y_f16;
     int n_stages;      // ring depth
     int64_t xs_bytes;  // one activation buffer
+    int x_bufs;        // 1 when every problem shares one x, else 2
     int tl_launch;     // APB_TIMELINE builds: launch index
 };
 
@@ -116,8 +118,8 @@ struct Geo {
     // layout: tables | lut x2 | ring | xs x2 | red | barriers
     static constexpr int kLut = (kTableBytes + 1023) / 1024 * 1024;
     static constexpr int kRing = kLut + 2 * kLutSlot;
-    static size_t total(int n_stages, int64_t xs_bytes) {
-        return (size_t)kRing + (size_t)n_stages * kStageBytes + 2 * (size_t)xs_bytes + kRedBytes + 16 * n_stages + 96;
+    static size_t total(int n_stages, int64_t xs_total) {
+        return (size_t)kRing + (size_t)n_stages * kStageBytes + (size_t)xs_total + kRedBytes + 16 * n_stages + 96;
     }
 };
 
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
     const uint32_t s_lut = saddr(smem + G::kLut);
     const uint32_t s_ring = saddr(smem + G::kRing);
     uint8_t* const xs = smem + G::kRing + (size_t)NST * G::kStageBytes;  // [2][m_x][padded] fp16
-    float* const red = reinterpret_cast<float*>(xs + 2 * L.xs_bytes);
+    float* const red = reinterpret_cast<float*>(xs + L.x_bufs * L.xs_bytes);
     const uint32_t bar = saddr(reinterpret_cast<uint8_t*>(red) + G::kRedBytes);
     // barriers (8 B each): full[NST] | empty[NST] | lut_full[2] | lut_empty[2] | table_ready[2] | item_done[2] | x_full[2]
     const uint32_t b_full = bar, b_empty = bar + 8 * NST, b_lfull = bar + 16 * NST, b_lempty = b_lfull + 16,
@@ -484,15 +486,18 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
             }
             if (jl < n_local) {
                 const int item = first + jl;
-                if (item >= pend) {  // next layer of a grouped launch (its x goes to the other buffer)
-                    pi = problem_of(L, item);
-                    pend = problem_end(L, pi);
-                    xb ^= 1;
-                    if (!waited) {
-                        asm volatile("griddepcontrol.wait;" ::: "memory");
-                        waited = true;
+                if (item >= pend) {  // next layer of a grouped launch
+                    const int npi = problem_of(L, item);
+                    pend = problem_end(L, npi);
+                    if (L.prob[npi].xid != L.prob[pi].xid) {  // new activations -> the other buffer
+                        xb = L.x_bufs == 2 ? xb ^ 1 : 0;
+                        if (!waited) {
+                            asm volatile("griddepcontrol.wait;" ::: "memory");
+                            waited = true;
+                        }
+                        issue_x(npi, xb);
                     }
-                    issue_x(pi, xb);
+                    pi = npi;
                 }
                 pi_hist[jl & 1] = pi;
                 mbar_wait(b_lfull + 8 * (jl & 1), (jl >> 1) & 1);
@@ -547,10 +552,13 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
         const int item = first + jl;
         bool new_x = jl == 0;
         if (item >= pend) {
-            pi = problem_of(L, item);
-            pend = problem_end(L, pi);
-            xb ^= 1;
-            new_x = true;
+            const int npi = problem_of(L, item);
+            pend = problem_end(L, npi);
+            if (L.prob[npi].xid != L.prob[pi].xid) {
+                xb = L.x_bufs == 2 ? xb ^ 1 : 0;
+                new_x = true;
+            }
+            pi = npi;
         }
         const Prob7& P = L.prob[pi];
         const int nt = P.n_tiles;
@@ -743,7 +751,7 @@ static int choose_cps(const Launch7& L) {
         return e ? std::atoi(e) : 0;
     }();
     if (forced == 1) return 1;
-    const bool fits2 = NB == 1 && Geo<K, NB, 2>::total(4, L.xs_bytes) <= kSmemLimit2;
+    const bool fits2 = NB == 1 && Geo<K, NB, 2>::total(4, L.x_bufs * L.xs_bytes) <= kSmemLimit2;
     if (forced == 2) return fits2 ? 2 : 1;
     // measured (tools/kbench): a win at k = 3 for every shape; at larger k only
     // for short launches (<= 2.5 items per SM), where cross-kernel overlap and
@@ -758,7 +766,7 @@ static int launch(Launch7& L, int flags, cudaStream_t s) {
     const size_t limit = CPS == 2 ? kSmemLimit2 : kSmemLimit;
     // ring depth: as many stages as fit (>= 3)
     int nst = kMaxStages;
-    while (nst >= G::kNG && G::total(nst, L.xs_bytes) > limit) --nst;
+    while (nst >= G::kNG && G::total(nst, L.x_bufs * L.xs_bytes) > limit) --nst;
     if (nst < G::kNG || nst < 3) return -1;
     L.n_stages = nst;
     auto kern = gemv7_kernel<K, NB, CPS>;
@@ -773,7 +781,7 @@ static int launch(Launch7& L, int flags, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3((unsigned)G::kThreads);
-    cfg.dynamicSmemBytes = G::total(nst, L.xs_bytes);
+    cfg.dynamicSmemBytes = G::total(nst, L.x_bufs * L.xs_bytes);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -841,6 +849,18 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     L.n_items = items;
     L.total_cost = cost;
     L.xs_bytes = (int64_t)m_x * max_tiles * 2048;
+    // activation identity: layers fed the same x (q/k/v, gate/up) stage it once
+    int n_xid = 0;
+    for (int i = 0; i < n; ++i) {
+        L.prob[i].xid = i;
+        for (int j = 0; j < i; ++j)
+            if (x[j] == x[i] && ldx[j] == ldx[i] && cols[j] == cols[i]) {
+                L.prob[i].xid = L.prob[j].xid;
+                break;
+            }
+        if (L.prob[i].xid == i) ++n_xid;
+    }
+    L.x_bufs = n_xid == 1 ? 1 : 2;
 #ifdef APB_TIMELINE
     L.tl_launch = g_tl_host_launch++;
 #endif
