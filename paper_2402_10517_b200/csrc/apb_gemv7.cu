@@ -32,6 +32,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -328,6 +329,76 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                      b_xfull + 8 * xb);
     };
 
+    // Lookup-table build for item slot `slot` from its LUT slot.  The service warp
+    // builds every table; the first one is built by the service and all compute
+    // warps together (they are idle until it exists).
+    // k >= 5: the first table (2^k single entries) is built by every compute warp
+    // with the service warp (measured: shortens the launch; for the pair tables of
+    // k <= 4 the extra code in the compute warps costs more than it saves)
+    constexpr bool kCoopFirst = K >= 5;
+    // coop: std::true_type for the shared first build (entries split over nbw warps)
+    auto build = [&](auto coop, int slot, int bw, int nbw) {  // builder bw of nbw warps
+        constexpr bool kCoop = decltype(coop)::value;
+        // table[entry][slot][lane]: lanes 4g..4g+3 = (row 2g, 2g, 2g+1, 2g+1) -> one
+        // 16-byte store per (entry, g) holds both copies of both rows.  Lane
+        // (e4 = lane >> 3, gg = lane & 7) writes entries e = e4 (mod 4) of rows 2gg, 2gg+1.
+        const int e4 = lane >> 3, gg = lane & 7, r0 = 2 * gg, r1 = r0 + 1;
+        const uint32_t lut = s_lut + slot * G::kLutSlot;
+        const uint32_t dst = saddr(smem) + slot * 128 + gg * 16;
+        if constexpr (G::kPair) {
+            uint32_t h0[1 << K], h1[1 << K];
+            constexpr int RB = (1 << K) * 2;  // LUT row bytes (16 or 32)
+#pragma unroll
+            for (int c = 0; c < RB / 16; ++c) {
+                const uint4 v0 = lds128(lut + r0 * RB + c * 16), v1 = lds128(lut + r1 * RB + c * 16);
+                const uint32_t a0[4] = {v0.x, v0.y, v0.z, v0.w}, a1[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    h0[c * 8 + i] = (i & 1) ? (a0[i >> 1] >> 16) : (a0[i >> 1] & 0xFFFFu);
+                    h1[c * 8 + i] = (i & 1) ? (a1[i >> 1] >> 16) : (a1[i >> 1] & 0xFFFFu);
+                }
+            }
+            // idx = 4i + e4: pair-index bits 0/1 (= code bit 0 of the even / odd
+            // column) come from e4, the rest from i (compile time)
+            constexpr int NH = 1 << (K - 1);
+            uint32_t s0[NH], s1[NH], o0[NH], o1[NH];
+#pragma unroll
+            for (int c = 0; c < NH; ++c) {
+                s0[c] = (e4 & 1) ? h0[2 * c + 1] : h0[2 * c];
+                s1[c] = (e4 & 1) ? h1[2 * c + 1] : h1[2 * c];
+                o0[c] = (e4 & 2) ? h0[2 * c + 1] : h0[2 * c];
+                o1[c] = (e4 & 2) ? h1[2 * c + 1] : h1[2 * c];
+            }
+#pragma unroll
+            for (int i = 0; i < G::kEntries / 4; ++i) {
+                if constexpr (kCoop)
+                    if (i % nbw != bw) continue;
+                uint32_t ce, co;
+                apb::pair_codes<K - 1>((uint32_t)i, ce, co);
+                const uint32_t v0 = s0[ce] | (o0[co] << 16), v1 = s1[ce] | (o1[co] << 16);
+                asm volatile("st.shared.v4.u32 [%0], {%1,%1,%2,%2};" ::"r"(dst + (4 * i + e4) * 256), "r"(v0), "r"(v1)
+                             : "memory");
+            }
+        } else {
+            auto chunk_addr = [&](int r, int cc) -> uint32_t {  // 16-byte chunk cc of LUT row r
+                const int b = cc / 8, ci = cc % 8;
+                if constexpr (K == 5) return lut + r * 64 + ((ci ^ ((r >> 1) & 3)) << 4);
+                else return lut + b * (kRows * 128) + r * 128 + ((ci ^ (r & 7)) << 4);
+            };
+#pragma unroll 2
+            for (int cc = e4 + (kCoop ? 4 * bw : 0); cc < G::kLutHalves / 8; cc += kCoop ? 4 * nbw : 4) {
+                const uint4 v0 = lds128(chunk_addr(r0, cc)), v1 = lds128(chunk_addr(r1, cc));
+                const uint32_t a0[4] = {v0.x, v0.y, v0.z, v0.w}, a1[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint32_t x0 = (i & 1) ? (a0[i >> 1] >> 16) : (a0[i >> 1] & 0xFFFFu);
+                    const uint32_t x1 = (i & 1) ? (a1[i >> 1] >> 16) : (a1[i >> 1] & 0xFFFFu);
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%2,%2};" ::"r"(dst + (cc * 8 + i) * 256), "r"(x0), "r"(x1)
+                                 : "memory");
+                }
+            }
+        }
+    };
     if (warp == WC) {
         // ============================ producer (TMA) ============================
         if (lane != 0) return;
@@ -370,65 +441,6 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
     if (warp == WC + 1) {
         // ========================= service: tables, x, y =========================
         const int g = lane >> 2, q = lane & 3, rho = 2 * g + (q >> 1);
-        auto build = [&](int slot) {
-            // table[entry][slot][lane]: lanes 4g..4g+3 = (row 2g, 2g, 2g+1, 2g+1) -> one
-            // 16-byte store per (entry, g) holds both copies of both rows.  Lane
-            // (e4 = lane >> 3, gg = lane & 7) writes entries e = e4 (mod 4) of rows 2gg, 2gg+1.
-            const int e4 = lane >> 3, gg = lane & 7, r0 = 2 * gg, r1 = r0 + 1;
-            const uint32_t lut = s_lut + slot * G::kLutSlot;
-            const uint32_t dst = saddr(smem) + slot * 128 + gg * 16;
-            if constexpr (G::kPair) {
-                uint32_t h0[1 << K], h1[1 << K];
-                constexpr int RB = (1 << K) * 2;  // LUT row bytes (16 or 32)
-#pragma unroll
-                for (int c = 0; c < RB / 16; ++c) {
-                    const uint4 v0 = lds128(lut + r0 * RB + c * 16), v1 = lds128(lut + r1 * RB + c * 16);
-                    const uint32_t a0[4] = {v0.x, v0.y, v0.z, v0.w}, a1[4] = {v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        h0[c * 8 + i] = (i & 1) ? (a0[i >> 1] >> 16) : (a0[i >> 1] & 0xFFFFu);
-                        h1[c * 8 + i] = (i & 1) ? (a1[i >> 1] >> 16) : (a1[i >> 1] & 0xFFFFu);
-                    }
-                }
-                // idx = 4i + e4: pair-index bits 0/1 (= code bit 0 of the even / odd
-                // column) come from e4, the rest from i (compile time)
-                constexpr int NH = 1 << (K - 1);
-                uint32_t s0[NH], s1[NH], o0[NH], o1[NH];
-#pragma unroll
-                for (int c = 0; c < NH; ++c) {
-                    s0[c] = (e4 & 1) ? h0[2 * c + 1] : h0[2 * c];
-                    s1[c] = (e4 & 1) ? h1[2 * c + 1] : h1[2 * c];
-                    o0[c] = (e4 & 2) ? h0[2 * c + 1] : h0[2 * c];
-                    o1[c] = (e4 & 2) ? h1[2 * c + 1] : h1[2 * c];
-                }
-#pragma unroll
-                for (int i = 0; i < G::kEntries / 4; ++i) {
-                    uint32_t ce, co;
-                    apb::pair_codes<K - 1>((uint32_t)i, ce, co);
-                    const uint32_t v0 = s0[ce] | (o0[co] << 16), v1 = s1[ce] | (o1[co] << 16);
-                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%2,%2};" ::"r"(dst + (4 * i + e4) * 256), "r"(v0), "r"(v1)
-                                 : "memory");
-                }
-            } else {
-                auto chunk_addr = [&](int r, int cc) -> uint32_t {  // 16-byte chunk cc of LUT row r
-                    const int b = cc / 8, ci = cc % 8;
-                    if constexpr (K == 5) return lut + r * 64 + ((ci ^ ((r >> 1) & 3)) << 4);
-                    else return lut + b * (kRows * 128) + r * 128 + ((ci ^ (r & 7)) << 4);
-                };
-#pragma unroll 2
-                for (int cc = e4; cc < G::kLutHalves / 8; cc += 4) {
-                    const uint4 v0 = lds128(chunk_addr(r0, cc)), v1 = lds128(chunk_addr(r1, cc));
-                    const uint32_t a0[4] = {v0.x, v0.y, v0.z, v0.w}, a1[4] = {v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const uint32_t x0 = (i & 1) ? (a0[i >> 1] >> 16) : (a0[i >> 1] & 0xFFFFu);
-                        const uint32_t x1 = (i & 1) ? (a1[i >> 1] >> 16) : (a1[i >> 1] & 0xFFFFu);
-                        asm volatile("st.shared.v4.u32 [%0], {%1,%1,%2,%2};" ::"r"(dst + (cc * 8 + i) * 256), "r"(x0), "r"(x1)
-                                     : "memory");
-                    }
-                }
-            }
-        };
         auto reduce = [&](int item, int pi, int slot) {
             const Prob7& P = L.prob[pi];
             const int m_out = L.x_split ? (L.m_x >> 1) : L.m_x;
@@ -501,7 +513,12 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                 }
                 pi_hist[jl & 1] = pi;
                 mbar_wait(b_lfull + 8 * (jl & 1), (jl >> 1) & 1);
-                build(jl & 1);
+                if (kCoopFirst && jl == 0) {
+                    build(std::true_type{}, 0, WC, WC + 1);
+                    asm volatile("bar.sync 1, %0;" ::"r"((WC + 1) * 32) : "memory");  // with the compute warps
+                } else {
+                    build(std::false_type{}, jl & 1, 0, 1);
+                }
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(b_lempty + 8 * (jl & 1));
@@ -583,7 +600,13 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
 #pragma unroll
             for (int c2 = 0; c2 < 2; ++c2) acc[b][c2][0] = acc[b][c2][1] = acc[b][c2][2] = acc[b][c2][3] = 0.f;
 
-        mbar_sleep(b_tready + 8 * (jl & 1), (jl >> 1) & 1);  // table of this item
+        if (kCoopFirst && jl == 0) {  // first table: built by all compute warps + the service warp
+            mbar_sleep(b_lfull, 0);
+            build(std::true_type{}, 0, warp, WC + 1);
+            asm volatile("bar.sync 1, %0;" ::"r"((WC + 1) * 32) : "memory");
+        } else {
+            mbar_sleep(b_tready + 8 * (jl & 1), (jl >> 1) & 1);  // table of this item
+        }
         if (new_x) {
             if constexpr (NB == 1) {  // activations of this layer staged
                 if (jl == 0 && warp == 0) {  // first layer: x / y of earlier kernels (PDL), then x
