@@ -594,11 +594,15 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                 xrow_g[b] = xlive[b] ? P.x + (int64_t)(2 * b + (g >> 2)) * P.ldx + xcol0 : g_zero_x;
         }
         const uint32_t off = (uint32_t)(jl & 1) * 128u + (uint32_t)lane * 4u;
-        float acc[NB][2][4];
+#ifndef APB7_ACC_CHAINS
+#define APB7_ACC_CHAINS 2
+#endif
+        constexpr int kAccChains = NB == 1 ? APB7_ACC_CHAINS : 2;  // independent HMMA accumulator chains
+        float acc[NB][kAccChains][4];
 #pragma unroll
         for (int b = 0; b < NB; ++b)
 #pragma unroll
-            for (int c2 = 0; c2 < 2; ++c2) acc[b][c2][0] = acc[b][c2][1] = acc[b][c2][2] = acc[b][c2][3] = 0.f;
+            for (int c2 = 0; c2 < kAccChains; ++c2) acc[b][c2][0] = acc[b][c2][1] = acc[b][c2][2] = acc[b][c2][3] = 0.f;
 
         if (kCoopFirst && jl == 0) {  // first table: built by all compute warps + the service warp
             mbar_sleep(b_lfull, 0);
@@ -628,62 +632,71 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
             mbar_sleep(b_full + 8 * slot, ph);
             if (warp == 0 && lane == 0 && gs == 0) APB_TL(3);
             const uint32_t sb = s_ring + slot * G::kStageBytes;
-            const bool xfull = tile < full_tiles;
+            // one tile of this warp's chunks; TAIL: the last, partial tile of a layer
+            // (activation columns >= cols read as zero) -- a separate instantiation, so
+            // full tiles carry no per-word-step tail test
+            auto run_tile = [&](auto tail) {
+                constexpr bool kTail = decltype(tail)::value;
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                uint2 pv[K];
+                for (int j = 0; j < 2; ++j) {
+                    uint2 pv[K];
 #pragma unroll
-                for (int p = 0; p < K; ++p) pv[K - 1 - p] = lds64(sb + p * 2048 + plane_off[j]);  // Q[i] = plane K-1-i
+                    for (int p = 0; p < K; ++p) pv[K - 1 - p] = lds64(sb + p * 2048 + plane_off[j]);  // Q[i] = plane K-1-i
 #pragma unroll
-                for (int wi = 0; wi < 2; ++wi) {
-                    const int cbase = tile * kTileWeights + 128 * j + 8 * wi;  // + 256p, relative to xcol0
+                    for (int wi = 0; wi < 2; ++wi) {
+                        const int cbase = tile * kTileWeights + 128 * j + 8 * wi;  // + 256p, relative to xcol0
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        uint32_t(&x8)[8] = xv[b];
-                        if constexpr (NB == 1) {
-                            const uint32_t xa = xrow_s + (uint32_t)cbase * 2u;
+                        for (int b = 0; b < NB; ++b) {
+                            uint32_t(&x8)[8] = xv[b];
+                            if constexpr (NB == 1) {
+                                const uint32_t xa = xrow_s + (uint32_t)cbase * 2u;
 #pragma unroll
-                            for (int p = 0; p < 4; ++p) lds64_keep(x8[2 * p], x8[2 * p + 1], xa + 512 * p, xlive[0]);
-                        } else {
+                                for (int p = 0; p < 4; ++p) lds64_keep(x8[2 * p], x8[2 * p + 1], xa + 512 * p, xlive[0]);
+                            } else {
 #pragma unroll
-                            for (int p = 0; p < 4; ++p) {
-                                const uint16_t* src = xrow_g[b] + cbase + 256 * p;
-                                if (!xfull && cbase + 256 * p >= xcols) src = g_zero_x;  // never read past ldx
-                                const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
-                                x8[2 * p] = v.x;
-                                x8[2 * p + 1] = v.y;
+                                for (int p = 0; p < 4; ++p) {
+                                    const uint16_t* src = xrow_g[b] + cbase + 256 * p;
+                                    if (kTail && cbase + 256 * p >= xcols) src = g_zero_x;  // never read past ldx
+                                    const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
+                                    x8[2 * p] = v.x;
+                                    x8[2 * p + 1] = v.y;
+                                }
+                            }
+                            if constexpr (kTail) {  // columns >= cols are zero
+#pragma unroll
+                                for (int p = 0; p < 4; ++p) {
+                                    const int c0 = cbase + 256 * p;
+                                    x8[2 * p] &= (c0 < xcols ? 0x0000FFFFu : 0u) | (c0 + 1 < xcols ? 0xFFFF0000u : 0u);
+                                    x8[2 * p + 1] &= (c0 + 2 < xcols ? 0x0000FFFFu : 0u) | (c0 + 3 < xcols ? 0xFFFF0000u : 0u);
+                                }
                             }
                         }
-                        if (!xfull) {  // tail tile: columns >= cols are zero
+                        uint32_t Q[K];
 #pragma unroll
-                            for (int p = 0; p < 4; ++p) {
-                                const int c0 = cbase + 256 * p;
-                                x8[2 * p] &= (c0 < xcols ? 0x0000FFFFu : 0u) | (c0 + 1 < xcols ? 0xFFFF0000u : 0u);
-                                x8[2 * p + 1] &= (c0 + 2 < xcols ? 0x0000FFFFu : 0u) | (c0 + 3 < xcols ? 0xFFFF0000u : 0u);
+                        for (int i = 0; i < K; ++i) Q[i] = wi ? pv[i].y : pv[i].x;
+                        uint32_t a[16];
+                        decode_word<K>(Q, off, a);
+                        if (j == 1 && wi == 0) {  // every plane register of the stage consumed: release it
+                            mbar_arrive(b_empty + 8 * slot);
+                            slot += NG;
+                            if (slot >= NST) {
+                                slot -= NST;
+                                ph ^= 1;
                             }
                         }
+#pragma unroll
+                        for (int b = 0; b < NB; ++b)
+#pragma unroll
+                            for (int p = 0; p < 4; ++p)
+                                mma16816(acc[b][kAccChains == 4 ? p : (p & 1)], a[p * 4 + 0], a[p * 4 + 2], a[p * 4 + 1],
+                                         a[p * 4 + 3], xv[b][2 * p], xv[b][2 * p + 1]);
                     }
-                    uint32_t Q[K];
-#pragma unroll
-                    for (int i = 0; i < K; ++i) Q[i] = wi ? pv[i].y : pv[i].x;
-                    uint32_t a[16];
-                    decode_word<K>(Q, off, a);
-                    if (j == 1 && wi == 0) {  // every plane register of the stage consumed: release it
-                        mbar_arrive(b_empty + 8 * slot);
-                        slot += NG;
-                        if (slot >= NST) {
-                            slot -= NST;
-                            ph ^= 1;
-                        }
-                    }
-#pragma unroll
-                    for (int b = 0; b < NB; ++b)
-#pragma unroll
-                        for (int p = 0; p < 4; ++p)
-                            mma16816(acc[b][p & 1], a[p * 4 + 0], a[p * 4 + 2], a[p * 4 + 1], a[p * 4 + 3],
-                                     xv[b][2 * p], xv[b][2 * p + 1]);
                 }
-            }
+            };
+            if (tile < full_tiles)
+                run_tile(std::false_type{});
+            else
+                run_tile(std::true_type{});
         }
         item_gs += nt;
         // rows 2g / 2g+1 of batch row 2b + (q>>1): D[g][2q'] + D[g+8][2q'+2] with q' = q & 2
@@ -691,7 +704,10 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
         for (int b = 0; b < NB; ++b) {
             float c[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) c[i] = acc[b][0][i] + acc[b][1][i];
+            for (int i = 0; i < 4; ++i) {
+                c[i] = acc[b][0][i] + acc[b][1][i];
+                if constexpr (kAccChains == 4) c[i] += acc[b][2][i] + acc[b][3][i];
+            }
             const float o2 = __shfl_xor_sync(0xffffffffu, c[2], 1), o3 = __shfl_xor_sync(0xffffffffu, c[3], 1);
             if ((q & 1) == 0) {
                 float* r = red + (jl & 1) * (WC * 2 * NB * kRows) + (warp * 2 * NB + 2 * b + (q >> 1)) * kRows + 2 * g;
