@@ -150,13 +150,14 @@ def make_layer_set(torch, seed: int, rank: int = 0, world: int = 1):
 
 
 def decode_plans(plan_mod, copies, pdl: bool):
-    """Per k: grouped q/k/v, o, grouped gate/up, down; weight copy rotated per launch."""
+    """Per k: grouped q/k/v, o, grouped gate/up, down; weight copy rotated per launch.
+    fp16 outputs (the metric's byte count, has M*R*2 output bytes)."""
     plans, i = [], 0
     for k in BITS:
         for grp in GROUPS:
             c = copies[i % len(copies)]
             p = plan_mod.GemvPlan([c[j] for j in grp], k, m=1, grouped=True, pdl=pdl,
-                                  shared_x=len(grp) > 1)
+                                  shared_x=len(grp) > 1, y_fp16=True)
             p.x[0].normal_()
             plans.append((k, grp, p))
             i += 1
