@@ -1130,7 +1130,7 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
         if (ldy[i] < rows[i]) return APB_ERR_SHAPE;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    if (m_x <= 4 && n_problems <= 16) {  // TMA-fed kernel (apb_gemv7.cu)
+    if (m_x <= 8 && n_problems <= 16) {  // TMA-fed kernel (apb_gemv7.cu)
         const int rc = apb7_try_gemv(n_problems, planes, n_max, rows, cols, padded_cols, k, lut, x, m_x, ldx, 0,
                                      x_split, y, y_dtype, ldy, 0, flags, stream);
         if (rc != -1) return rc;

@@ -99,7 +99,12 @@ template <int K, int NB = 1, int CPS = 1>
 struct Geo {
     static constexpr bool kPair = K <= 4;
     static constexpr int kEntries = kPair ? (1 << (2 * K)) : (1 << K);
-    static constexpr int kTableBytes = kEntries * 256;  // [entry][slot 2][lane 32] u32
+    // NB == 4: "batch-in-N" mapping (lane owns rows g and g+8, 4 copies per row,
+    // up to 8 batch rows in the MMA N dimension); its table is
+    // [slot (64 KB stride)][entry][row-half 2][lane 32] u32.  Otherwise the
+    // row-copy mapping: [entry][slot 2][lane 32] u32.
+    static constexpr bool kMapN = NB == 4;
+    static constexpr int kTableBytes = kMapN ? 65536 + kEntries * 256 : kEntries * 256;
     static constexpr int kLutHalves = 1 << K;
     static constexpr int kLutBox = kLutHalves < 64 ? kLutHalves : 64;  // halves per box row
     static constexpr int kLutBoxes = kLutHalves / kLutBox;
@@ -111,7 +116,7 @@ struct Geo {
 #else
     // compute warps, groups of 4 (measured best per k; 8 for 4 batch pairs: registers;
     // 8 when two CTAs share an SM)
-    static constexpr int kWC = (NB >= 4 || CPS == 2) ? 8 : (K == 8 ? 12 : 16);
+    static constexpr int kWC = NB == 4 ? 12 : (CPS == 2 ? 8 : (K == 8 ? 12 : 16));
 #endif
     static constexpr int kNG = kWC / 4;
     static constexpr int kThreads = (kWC + 2) * 32;
@@ -335,10 +340,68 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
     // k >= 5: the first table (2^k single entries) is built by every compute warp
     // with the service warp (measured: shortens the launch; for the pair tables of
     // k <= 4 the extra code in the compute warps costs more than it saves)
-    constexpr bool kCoopFirst = K >= 5;
+    constexpr bool kCoopFirst = K >= 5 && !G::kMapN;
     // coop: std::true_type for the shared first build (entries split over nbw warps)
     auto build = [&](auto coop, int slot, int bw, int nbw) {  // builder bw of nbw warps
         constexpr bool kCoop = decltype(coop)::value;
+        if constexpr (G::kMapN) {
+            // rows gg (half 0) and gg+8 (half 1), 4 copies each: one STS.128 per (entry, half)
+            const int e4 = lane >> 3, gg = lane & 7, r0 = gg, r1 = gg + 8;
+            const uint32_t lut = s_lut + slot * G::kLutSlot;
+            const uint32_t dst = saddr(smem) + slot * 65536 + gg * 16;
+            if constexpr (G::kPair) {
+                uint32_t h0[1 << K], h1[1 << K];
+                constexpr int RB = (1 << K) * 2;
+#pragma unroll
+                for (int c = 0; c < RB / 16; ++c) {
+                    const uint4 v0 = lds128(lut + r0 * RB + c * 16), v1 = lds128(lut + r1 * RB + c * 16);
+                    const uint32_t a0[4] = {v0.x, v0.y, v0.z, v0.w}, a1[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        h0[c * 8 + i] = (i & 1) ? (a0[i >> 1] >> 16) : (a0[i >> 1] & 0xFFFFu);
+                        h1[c * 8 + i] = (i & 1) ? (a1[i >> 1] >> 16) : (a1[i >> 1] & 0xFFFFu);
+                    }
+                }
+                constexpr int NH = 1 << (K - 1);
+                uint32_t s0[NH], s1[NH], o0[NH], o1[NH];
+#pragma unroll
+                for (int c = 0; c < NH; ++c) {
+                    s0[c] = (e4 & 1) ? h0[2 * c + 1] : h0[2 * c];
+                    s1[c] = (e4 & 1) ? h1[2 * c + 1] : h1[2 * c];
+                    o0[c] = (e4 & 2) ? h0[2 * c + 1] : h0[2 * c];
+                    o1[c] = (e4 & 2) ? h1[2 * c + 1] : h1[2 * c];
+                }
+#pragma unroll
+                for (int i = 0; i < G::kEntries / 4; ++i) {
+                    uint32_t ce, co;
+                    apb::pair_codes<K - 1>((uint32_t)i, ce, co);
+                    const uint32_t v0 = s0[ce] | (o0[co] << 16), v1 = s1[ce] | (o1[co] << 16);
+                    const uint32_t a = dst + (4 * i + e4) * 256;
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(a), "r"(v0) : "memory");
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(a + 128), "r"(v1) : "memory");
+                }
+            } else {
+                auto chunk_addr = [&](int r, int cc) -> uint32_t {
+                    const int b = cc / 8, ci = cc % 8;
+                    if constexpr (K == 5) return lut + r * 64 + ((ci ^ ((r >> 1) & 3)) << 4);
+                    else return lut + b * (kRows * 128) + r * 128 + ((ci ^ (r & 7)) << 4);
+                };
+#pragma unroll 2
+                for (int cc = e4; cc < G::kLutHalves / 8; cc += 4) {
+                    const uint4 v0 = lds128(chunk_addr(r0, cc)), v1 = lds128(chunk_addr(r1, cc));
+                    const uint32_t a0[4] = {v0.x, v0.y, v0.z, v0.w}, a1[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const uint32_t x0 = (i & 1) ? (a0[i >> 1] >> 16) : (a0[i >> 1] & 0xFFFFu);
+                        const uint32_t x1 = (i & 1) ? (a1[i >> 1] >> 16) : (a1[i >> 1] & 0xFFFFu);
+                        const uint32_t a = dst + (cc * 8 + i) * 256;
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(a), "r"(x0) : "memory");
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(a + 128), "r"(x1) : "memory");
+                    }
+                }
+            }
+            return;
+        } else {
         // table[entry][slot][lane]: lanes 4g..4g+3 = (row 2g, 2g, 2g+1, 2g+1) -> one
         // 16-byte store per (entry, g) holds both copies of both rows.  Lane
         // (e4 = lane >> 3, gg = lane & 7) writes entries e = e4 (mod 4) of rows 2gg, 2gg+1.
@@ -397,6 +460,7 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                                  : "memory");
                 }
             }
+        }
         }
     };
     if (warp == WC) {
@@ -532,6 +596,109 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
     }
 
     // =============================== compute warps ===============================
+    if constexpr (G::kMapN) {
+        // Batch-in-N mapping: lane (g, q) owns rows g (A rows g) and g + 8 (A rows
+        // g + 8) at the same columns; its 16-B chunk c = su + 4(q>>1), 8-B half q&1
+        // (words 4c + 2(q&1) + wi); B column n = batch row n (dense: every lane loads
+        // x[min(g, m_x-1)] for its columns from L1-resident global memory).
+        const int g = lane >> 2, q = lane & 3;
+        const int grp = warp >> 2, su = warp & 3;
+        const int c = su + 4 * (q >> 1), hf = q & 1;
+        const uint32_t po0 = g * 128 + ((c ^ g) << 4) + hf * 8, po1 = po0 + 8 * 128;  // rows g, g+8 (same swizzle)
+        const int gm = g < L.m_x ? g : L.m_x - 1;
+        const int xcol0 = 8 * (4 * c + 2 * hf);  // column of word wi=0, p=0 (+ tile*1024 + 256p + 8wi)
+        int pi = problem_of(L, first), pend = problem_end(L, pi);
+        int gs = grp, item_gs = 0, slot = grp, ph = 0;
+#pragma unroll 1
+        for (int jl = 0; jl < n_local; ++jl) {
+            const int item = first + jl;
+            if (item >= pend) {
+                pi = problem_of(L, item);
+                pend = problem_end(L, pi);
+            }
+            const Prob7& P = L.prob[pi];
+            const int nt = P.n_tiles;
+            const uint16_t* const xrow = P.x + (int64_t)gm * P.ldx + xcol0;
+            const int xcols = (int)P.cols - xcol0;
+            const int full_tiles = (int)(P.cols / kTileWeights);
+            const uint32_t off0 = ((uint32_t)(jl & 1) << 16) | ((uint32_t)lane * 4u), off1 = off0 + 128u;
+            float acc[2][4];
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2) acc[c2][0] = acc[c2][1] = acc[c2][2] = acc[c2][3] = 0.f;
+            mbar_sleep(b_tready + 8 * (jl & 1), (jl >> 1) & 1);
+            if (jl == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // x from the previous kernel
+#pragma unroll 1
+            for (; gs < item_gs + nt; gs += NG) {
+                const int tile = gs - item_gs;
+                mbar_sleep(b_full + 8 * slot, ph);
+                const uint32_t sb = s_ring + slot * G::kStageBytes;
+                auto run_tile = [&](auto tail) {
+                    constexpr bool kTail = decltype(tail)::value;
+                    uint2 pa[K], pb[K];
+#pragma unroll
+                    for (int p = 0; p < K; ++p) {
+                        pa[K - 1 - p] = lds64(sb + p * 2048 + po0);
+                        pb[K - 1 - p] = lds64(sb + p * 2048 + po1);
+                    }
+#pragma unroll
+                    for (int wi = 0; wi < 2; ++wi) {
+                        const int cbase = tile * kTileWeights + 8 * wi;  // + 256p, relative to xcol0
+                        uint4 xq[4];
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) {
+                            const int c0 = cbase + 256 * p;
+                            const uint16_t* src = xrow + c0;
+                            if (kTail && c0 >= xcols) src = g_zero_x;  // never read past ldx
+                            xq[p] = __ldg(reinterpret_cast<const uint4*>(src));
+                            if constexpr (kTail) {
+                                uint32_t w[4] = {xq[p].x, xq[p].y, xq[p].z, xq[p].w};
+#pragma unroll
+                                for (int h = 0; h < 4; ++h)
+                                    w[h] &= (c0 + 2 * h < xcols ? 0x0000FFFFu : 0u) | (c0 + 2 * h + 1 < xcols ? 0xFFFF0000u : 0u);
+                                xq[p] = make_uint4(w[0], w[1], w[2], w[3]);
+                            }
+                        }
+                        uint32_t Qa[K], Qb[K];
+#pragma unroll
+                        for (int i = 0; i < K; ++i) {
+                            Qa[i] = wi ? pa[i].y : pa[i].x;
+                            Qb[i] = wi ? pb[i].y : pb[i].x;
+                        }
+                        uint32_t a0[16], a1[16];
+                        decode_word<K>(Qa, off0, a0);
+                        decode_word<K>(Qb, off1, a1);
+                        if (wi == 0) {  // every plane register of the stage consumed: release it
+                            mbar_arrive(b_empty + 8 * slot);
+                            slot += NG;
+                            if (slot >= NST) {
+                                slot -= NST;
+                                ph ^= 1;
+                            }
+                        }
+#pragma unroll
+                        for (int p = 0; p < 4; ++p)
+#pragma unroll
+                            for (int jj = 0; jj < 2; ++jj)
+                                mma16816(acc[p & 1], a0[p * 4 + 2 * jj], a1[p * 4 + 2 * jj], a0[p * 4 + 2 * jj + 1],
+                                         a1[p * 4 + 2 * jj + 1], u4w(xq[p], 2 * jj), u4w(xq[p], 2 * jj + 1));
+                    }
+                };
+                if (tile < full_tiles)
+                    run_tile(std::false_type{});
+                else
+                    run_tile(std::true_type{});
+            }
+            item_gs += nt;
+            // D[g][2q..2q+1] / D[g+8][2q..2q+1]: rows g, g+8 of batch rows 2q, 2q+1
+            float* r = red + (jl & 1) * (WC * 8 * kRows) + warp * 8 * kRows;
+            r[(2 * q) * kRows + g] = acc[0][0] + acc[1][0];
+            r[(2 * q + 1) * kRows + g] = acc[0][1] + acc[1][1];
+            r[(2 * q) * kRows + g + 8] = acc[0][2] + acc[1][2];
+            r[(2 * q + 1) * kRows + g + 8] = acc[0][3] + acc[1][3];
+            mbar_arrive(b_idone + 8 * (jl & 1));
+        }
+        return;
+    }
     // Lane (g, q): row rho = 2g + (q >> 1) of the item, copy cp = q & 1.  Warp su
     // = warp & 3 of its group takes 16-byte chunks su and su + 4 of every stage
     // (tile) row; copy cp reads words 2cp, 2cp+1 of a chunk (LDS.64: rows 0..7 of a
@@ -852,9 +1019,9 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
         const char* e = std::getenv("APB_GEMV_V7");
         return e && e[0] == '0';
     }();
-    // batch rows <= 4 (measured: for 5..8 rows the 16-row mapping of apb_gemv.cu,
-    // which carries the batch in the MMA N dimension, is faster)
-    if (disabled || k < 3 || k > 8 || m_x > 4 || n > kMaxProb) return -1;
+    // batch rows: <= 2 row-copy mapping (x in smem), 3..8 batch-in-N mapping
+    // (measured faster than the two-batch-pair row-copy path from 3 rows up)
+    if (disabled || k < 3 || k > 8 || m_x > 8 || n > kMaxProb) return -1;
     for (int i = 0; i < n; ++i)
         if (padded[i] > kMaxCols) return -1;
     static thread_local Launch7 L;  // ~5 KB: kept off the stack
@@ -904,13 +1071,17 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     L.tl_launch = g_tl_host_launch++;
 #endif
     cudaStream_t s = (cudaStream_t)stream;
-    const int nb = m_x <= 2 ? 1 : 2;
+#ifndef APB7_NB2_MAX
+#define APB7_NB2_MAX 2
+#endif
+    const int nb = m_x <= 2 ? 1 : (m_x <= APB7_NB2_MAX ? 2 : 4);
     if (nb > 1) L.xs_bytes = 0;
     switch (k * 8 + nb) {
 #define APB7_CASE(K)                                                                                  \
     case K * 8 + 1:                                                                                   \
         return choose_cps<K, 1>(L) == 2 ? launch<K, 1, 2>(L, flags, s) : launch<K, 1, 1>(L, flags, s); \
-    case K * 8 + 2: return launch<K, 2, 1>(L, flags, s);
+    case K * 8 + 2: return launch<K, 2, 1>(L, flags, s);                                               \
+    case K * 8 + 4: return launch<K, 4, 1>(L, flags, s);
         APB7_CASE(3)
         APB7_CASE(4)
         APB7_CASE(5)
