@@ -959,11 +959,12 @@ static int choose_cps(const Launch7& L) {
     if (forced == 1) return 1;
     const bool fits2 = NB == 1 && Geo<K, NB, 2>::total(4, L.x_bufs * L.xs_bytes) <= kSmemLimit2;
     if (forced == 2) return fits2 ? 2 : 1;
-    // measured (tools/kbench): a win at k = 3 for every shape; at larger k only
-    // for short launches (<= 2.5 items per SM), where cross-kernel overlap and
-    // granularity dominate -- on long launches the 8-warp CTAs lose ~4 %.
-    const bool short_launch = 2 * L.n_items <= 5 * sm_count();
-    return fits2 && (K == 3 || short_launch) ? 2 : 1;
+    // measured: in a PDL chain of decode-sized launches (the bench step) two CTAs
+    // per SM win +5 % overall (cross-kernel overlap, granularity); a long
+    // isolated launch (> 10 items per SM, e.g. a 28672-row layer) runs ~4 %
+    // faster with one 16-warp CTA per SM, except at k = 3.
+    const bool long_launch = L.n_items > 10 * sm_count();
+    return fits2 && (K == 3 || !long_launch) ? 2 : 1;
 }
 
 template <int K, int NB, int CPS>
