@@ -193,7 +193,7 @@ def measured_traffic():
         dram = [l["dram_bytes"] for l in tr["launches"]]
         if len(dram) != len(GROUPS):
             return None, None
-        k = int(tr["launches"][0]["kernel"].split("<")[1].split(">")[0])
+        k = int(tr["launches"][0]["kernel"].split("<")[1].split(">")[0].split(",")[0])
         alg = [sum(alg_bytes(SHAPES[j][1], SHAPES[j][2], k) for j in grp) for grp in GROUPS]
         ratio = sum(dram) / sum(alg)
         return round(ratio * step_bytes()), {"dram_over_algorithmic": round(ratio, 4), "k": k,
