@@ -482,3 +482,25 @@ def test_step_plan_host_roundtrip(api):
     assert torch.equal(y[0][0], engine.gemv(preps[0], x0, cfg3))
     assert torch.equal(y[1][0], engine.gemv(preps[1], x0, cfg3))
     assert torch.equal(y[2][0], engine.gemv(preps[2], x1, cfg8))
+
+
+@pytest.mark.parametrize("shape", [(333, 1500), (17, 300), (1000, 11008), (4096, 3000)])
+def test_tma_kernel_paths_vs_oracle(api, shape):
+    # every dispatch path of the TMA-fed kernel (csrc/apb_gemv7.cu) against the C
+    # oracle: row-copy mapping (1-2 activation rows; fp32 x = hi/lo pair), batch-in-N
+    # mapping (3..8 rows), one or two CTAs per SM (small / large launches), ragged
+    # rows (rows % 16 != 0), tail tiles (cols % 1024 != 0, odd column counts)
+    _, _, engine, _ = api
+    rows, cols = shape
+    layer = _random_layer(api, 7 + rows, rows, cols)
+    prep = engine.prepare(layer)
+    planes = prep.planes.cpu().numpy()
+    rng = np.random.default_rng(rows * 31 + cols)
+    for k in (3, 4, 5, 8):
+        for m, fp16 in ((1, True), (1, False), (2, True), (3, True), (4, False), (5, True), (8, True)):
+            x = rng.standard_normal((m, cols))
+            cfg = engine.GemvConfig(bit_width=k, activations_fp16=fp16, dense_threshold=16)
+            y = engine.gemm(prep, x, cfg)
+            want = ora.gemm(planes, cols, k, layer.centroid_tables[k], ora.prep_x(x, cols, fp16))
+            err = ora.rel_err(y, want)
+            assert err < TOL, (shape, k, m, fp16, err)
