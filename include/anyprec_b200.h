@@ -137,6 +137,24 @@ int apb_rope_cache(const uint16_t* q, const uint16_t* k, const uint16_t* v, cons
                    int64_t cache_head_stride, void* stream);
 int apb_silu_mul(const uint16_t* gate, const uint16_t* up, uint16_t* out, int64_t n, void* stream);
 
+/* Single-query decode attention with RoPE and KV-cache append fused in
+ * (head_dim 128).  q, k, v: this token's projections (heads x head_dim fp16);
+ * k_cache / v_cache: row 0 of head 0, heads `cache_head_stride` elements apart;
+ * rows 0..pos-1 hold the past, the rotated k and v of this token are written to
+ * row pos, and out[h] = softmax(scale * rot(q_h) . K_h[0..pos]) V_h[0..pos]
+ * (fp16, heads x head_dim).  workspace: >= apb_attention_decode_workspace(
+ * heads, head_dim, pos + 1) bytes, zero-filled once before first use (the
+ * kernel leaves it reusable).  next_k_cache / next_v_cache (NULL or both set,
+ * same geometry): the next block's cache, whose rows 0..pos are prefetched into
+ * L2 for its own attention call.  Launched with programmatic stream
+ * serialisation like the GEMVs. */
+int64_t apb_attention_decode_workspace(int heads, int head_dim, int64_t max_keys);
+int apb_attention_decode(const uint16_t* q, const uint16_t* k, const uint16_t* v, const float* cosv,
+                         const float* sinv, uint16_t* k_cache, uint16_t* v_cache, int heads, int head_dim,
+                         int64_t cache_head_stride, int pos, float scale, void* workspace,
+                         int64_t workspace_bytes, uint16_t* out, const uint16_t* next_k_cache,
+                         const uint16_t* next_v_cache, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -183,6 +183,28 @@ __device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap* m, int c0,
         "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
         : "memory");
 }
+// Plane tiles are read exactly once per call: evict-first keeps them from
+// displacing what IS reused from L2 (centroid rows, x, a decode step's KV cache).
+#ifndef APB7_EVICT_FIRST
+#define APB7_EVICT_FIRST 1
+#endif
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma3_ef(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, uint32_t bar,
+                                        uint64_t pol) {
+#if APB7_EVICT_FIRST
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+        "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
+        : "memory");
+#else
+    (void)pol;
+    tma3(dst, m, c0, c1, c2, bar);
+#endif
+}
 __device__ __forceinline__ void tma2(uint32_t dst, const CUtensorMap* m, int c0, int c1, uint32_t bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
@@ -466,6 +488,7 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
     if (warp == WC) {
         // ============================ producer (TMA) ============================
         if (lane != 0) return;
+        const uint64_t pol = policy_evict_first();
         int slot = 0, ph = 0;  // ring position of the next stage
         int pi = problem_of(L, first), pend = problem_end(L, pi);
 #pragma unroll 1
@@ -491,7 +514,8 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                 mbar_expect_tx(b_full + 8 * slot, G::kStageBytes);
                 const uint32_t dst = s_ring + slot * G::kStageBytes;
 #pragma unroll
-                for (int p = 0; p < K; ++p) tma3(dst + p * 2048, &L.tm_planes[pi], t * kTileBytes, row0, p, b_full + 8 * slot);
+                for (int p = 0; p < K; ++p)
+                    tma3_ef(dst + p * 2048, &L.tm_planes[pi], t * kTileBytes, row0, p, b_full + 8 * slot, pol);
                 if (++slot == NST) {
                     slot = 0;
                     ++ph;

@@ -6,9 +6,10 @@ the reference lists the same seven per block) is one n_max-bit bitplane parent
 served at a per-step bit-width k through the B200 GEMV (plan.GemvPlan, grouped
 q/k/v and gate/up launches, fp16 outputs, PDL chain).  The glue around them is
 three fused sm_100a kernels of csrc/apb_decode.cu (residual add + RMSNorm
-writing the next GEMV's activation buffer, RoPE + KV-cache append, SiLU*up) plus
-PyTorch's SDPA for attention over the cache and a cuBLAS fp16 LM head; the
-whole step is captured in one CUDA graph per k.  Weights are random-init (codes uniform in [0, 2^n_max),
+writing the next GEMV's activation buffer; RoPE + KV-cache append + split-chunk
+single-query attention writing the o-projection's activation buffer; SiLU*up),
+all in the GEMVs' PDL chain, plus a cuBLAS fp16 LM head; the whole step is
+captured in one CUDA graph per k.  Weights are random-init (codes uniform in [0, 2^n_max),
 sorted N(0,1) centroid rows, helpers.random_layer semantics), activations are
 real (embedding lookup of a token id, norms with unit weights).
 
@@ -58,6 +59,7 @@ class DecodeModel:
     def __init__(self, cfg: LlamaConfig = LlamaConfig(), context: int = 1024, seed: int = 0):
         torch = dev.require_cuda()
         from . import engine, plan
+        from ._lib import load
 
         self.cfg, self.context = cfg, context
         H, I, nh, hd = cfg.hidden, cfg.intermediate, cfg.heads, cfg.head_dim
@@ -79,10 +81,12 @@ class DecodeModel:
         ang = float(context) * inv
         self.cos, self.sin = torch.cos(ang).contiguous(), torch.sin(ang).contiguous()
         self.resid = torch.zeros(H, device="cuda", dtype=torch.float32)
-        self.qbuf = torch.zeros(nh * hd, device="cuda", dtype=torch.float16)
+        ws_bytes = load().apb_attention_decode_workspace(nh, hd, context + 1)
+        self.attn_ws = torch.zeros(ws_bytes, device="cuda", dtype=torch.uint8)
         self.hbuf = torch.zeros(1, H, device="cuda", dtype=torch.float16)
         self.token = torch.zeros(1, dtype=torch.long, device="cuda")
         self.next_token = torch.zeros(1, dtype=torch.long, device="cuda")
+        self.kv_prefetch = True
         self._plans, self._graphs = {}, {}
         self._plan_mod = plan
 
@@ -117,12 +121,11 @@ class DecodeModel:
             check(lib.apb_rms_residual(P(self.resid), add, P(self.norm_w), P(qkv.x[0]), H, 1e-5, st),
                   "apb_rms_residual")
             qkv.run()
-            kc, vc = self.k_cache[li], self.v_cache[li]
-            check(lib.apb_rope_cache(P(qkv.y[0]), P(qkv.y[1]), P(qkv.y[2]), P(self.cos), P(self.sin),
-                                     P(self.qbuf), P(kc) + ctx * hd * 2, P(vc) + ctx * hd * 2, nh, hd,
-                                     (ctx + 1) * hd, st), "apb_rope_cache")
-            att = torch.nn.functional.scaled_dot_product_attention(self.qbuf.view(1, nh, 1, hd), kc, vc)
-            o.x[0][:, :H].copy_(att.view(1, H))
+            check(lib.apb_attention_decode(P(qkv.y[0]), P(qkv.y[1]), P(qkv.y[2]), P(self.cos), P(self.sin),
+                                           P(self.k_cache[li]), P(self.v_cache[li]), nh, hd, (ctx + 1) * hd, ctx,
+                                           hd ** -0.5, P(self.attn_ws), self.attn_ws.numel(), P(o.x[0]),
+                                           *self._next_kv(li), st),
+                  "apb_attention_decode")
             o.run()
             check(lib.apb_rms_residual(P(self.resid), P(o.y[0]), P(self.norm_w), P(gu.x[0]), H, 1e-5, st),
                   "apb_rms_residual")
@@ -134,6 +137,12 @@ class DecodeModel:
               "apb_rms_residual")
         logits = self.hbuf @ self.lm_head.t()
         self.next_token.copy_(torch.argmax(logits, dim=-1))
+
+    def _next_kv(self, li):
+        """The next block's cache for the attention kernel's L2 prefetch (none after the last)."""
+        if li + 1 >= self.cfg.layers or not self.kv_prefetch:
+            return None, None
+        return dev.ptr(self.k_cache[li + 1]), dev.ptr(self.v_cache[li + 1])
 
     def capture(self, k: int):
         torch = dev.require_cuda()

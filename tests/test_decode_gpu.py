@@ -58,3 +58,98 @@ def test_decode_step_matches_dequantized_reference():
         model.step(k)
         torch.cuda.synchronize()
         assert torch.equal(model.hbuf.float().view(-1), got), k
+
+
+@pytest.mark.parametrize("heads,pos", [(1, 0), (4, 1), (4, 63), (4, 64), (32, 200), (32, 1024), (8, 4095)])
+def test_attention_decode_vs_fp32(heads, pos):
+    """apb_attention_decode (RoPE + cache append + split-chunk attention) against
+    fp32 torch on the same fp16 inputs; twice in a row gives the same bits (the
+    per-head tickets reset themselves)."""
+    import torch
+
+    from paper_2402_10517_b200 import _device as dev
+    from paper_2402_10517_b200._lib import check, load
+
+    lib, hd = load(), 128
+    g = torch.Generator(device="cuda").manual_seed(pos * 7 + heads)
+    stride = (pos + 1 + 5) * hd  # slack rows after pos: must stay untouched
+    q, k, v = (torch.randn(heads * hd, device="cuda", generator=g).half() for _ in range(3))
+    kc = torch.randn(heads * stride, device="cuda", generator=g).half()
+    vc = torch.randn(heads * stride, device="cuda", generator=g).half()
+    kc0, vc0 = kc.clone(), vc.clone()
+    ang = (pos + 1.5) / (10000.0 ** (torch.arange(0, hd, 2, device="cuda").float() / hd))
+    cos, sin = torch.cos(ang).contiguous(), torch.sin(ang).contiguous()
+    nbytes = lib.apb_attention_decode_workspace(heads, hd, pos + 1)
+    ws = torch.zeros(nbytes, device="cuda", dtype=torch.uint8)
+    nxt = torch.randn(2, heads * stride, device="cuda", generator=g).half()  # prefetch target only
+    outs = []
+    for _ in range(2):
+        out = torch.empty(heads * hd, device="cuda", dtype=torch.float16)
+        P = dev.ptr
+        check(lib.apb_attention_decode(P(q), P(k), P(v), P(cos), P(sin), P(kc), P(vc), heads, hd, stride, pos,
+                                       hd ** -0.5, P(ws), nbytes, P(out), P(nxt[0]), P(nxt[1]), dev.stream_ptr()),
+              "apb_attention_decode")
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+
+    def rope(t):
+        a, b = t[:, : hd // 2], t[:, hd // 2:]
+        return torch.cat([a * cos - b * sin, b * cos + a * sin], dim=-1)
+
+    qr = rope(q.float().view(heads, hd))
+    kr = rope(k.float().view(heads, hd)).half()
+    K = kc0.view(heads, -1, hd)[:, : pos + 1].float().clone()
+    V = vc0.view(heads, -1, hd)[:, : pos + 1].float().clone()
+    K[:, pos], V[:, pos] = kr.float(), v.float().view(heads, hd)
+    att = torch.softmax((qr.unsqueeze(1) @ K.transpose(1, 2)) * hd ** -0.5, dim=-1) @ V
+    want = att.view(-1)
+    err = float((outs[0].float() - want).abs().max())
+    assert err < 2e-3, err
+    # cache: row pos now holds rot(k) / v; every other row untouched
+    kcv, vcv = kc.view(heads, -1, hd), vc.view(heads, -1, hd)
+    assert torch.equal(kcv[:, pos], kr) and torch.equal(vcv[:, pos], v.view(heads, hd))
+    mask = torch.ones(kcv.shape[1], dtype=torch.bool, device="cuda")
+    mask[pos] = False
+    assert torch.equal(kcv[:, mask], kc0.view(heads, -1, hd)[:, mask])
+    assert torch.equal(vcv[:, mask], vc0.view(heads, -1, hd)[:, mask])
+
+
+def test_attention_decode_rejects_bad_arguments():
+    from paper_2402_10517_b200._lib import load
+
+    lib = load()
+    assert lib.apb_attention_decode_workspace(4, 64, 10) == -1
+    assert lib.apb_attention_decode_workspace(4, 128, 0) == -1
+
+
+@pytest.mark.parametrize("n", [4096, 4097, 11008, 20000])
+def test_rms_residual_and_silu_vs_fp32(n):
+    """Vector (n % 4 == 0, n <= 16K) and scalar paths of the RMS kernel, with and
+    without the residual add; SiLU*up at even and odd n."""
+    import torch
+
+    from paper_2402_10517_b200 import _device as dev
+    from paper_2402_10517_b200._lib import check, load
+
+    lib, P, st = load(), dev.ptr, dev.stream_ptr()
+    g = torch.Generator(device="cuda").manual_seed(n)
+    resid = torch.randn(n, device="cuda", generator=g)
+    add = torch.randn(n, device="cuda", generator=g).half()
+    w = (torch.rand(n, device="cuda", generator=g) + 0.5).half()
+    for use_add in (False, True):
+        r = resid.clone()
+        out = torch.empty(n, device="cuda", dtype=torch.float16)
+        check(lib.apb_rms_residual(P(r), P(add) if use_add else None, P(w), P(out), n, 1e-5, st),
+              "apb_rms_residual")
+        torch.cuda.synchronize()
+        want_r = resid + add.float() if use_add else resid
+        assert torch.allclose(r, want_r, rtol=0, atol=1e-6)
+        want = want_r * torch.rsqrt(want_r.pow(2).mean() + 1e-5) * w.float()
+        assert float((out.float() - want).abs().max()) < 4e-3
+    gate, up = (torch.randn(n, device="cuda", generator=g).half() for _ in range(2))
+    out = torch.empty(n, device="cuda", dtype=torch.float16)
+    check(lib.apb_silu_mul(P(gate), P(up), P(out), n, st), "apb_silu_mul")
+    torch.cuda.synchronize()
+    want = torch.nn.functional.silu(gate.float()) * up.float()
+    assert float((out.float() - want).abs().max()) < 1e-2
