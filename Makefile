@@ -3,7 +3,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
 PKG := paper_2402_10517_b200
-SRCS := $(PKG)/csrc/apb_abi.cu $(PKG)/csrc/apb_bitplane.cu $(PKG)/csrc/apb_gemv.cu $(PKG)/csrc/apb_gemv7.cu $(PKG)/csrc/apb_decode.cu
+SRCS := $(PKG)/csrc/apb_abi.cu $(PKG)/csrc/apb_bitplane.cu $(PKG)/csrc/apb_gemv.cu $(PKG)/csrc/apb_gemv7.cu $(PKG)/csrc/apb_decode.cu $(PKG)/csrc/apb_quant.cu
 OBJS := $(SRCS:.cu=.o)
 LIB := $(PKG)/libanyprec_b200.so
 
@@ -11,6 +11,9 @@ all: $(LIB) oracle/liboracle.so
 
 $(PKG)/csrc/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/apb_common.cuh include/anyprec_b200.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+
+# the quantizer is bit-exact with the reference's float64 numpy arithmetic: no FMA contraction
+$(PKG)/csrc/apb_quant.o: NVFLAGS += -fmad=false
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart

@@ -155,6 +155,26 @@ int apb_attention_decode(const uint16_t* q, const uint16_t* k, const uint16_t* v
                          int64_t workspace_bytes, uint16_t* out, const uint16_t* next_k_cache,
                          const uint16_t* next_v_cache, void* stream);
 
+/* ---- offline quantizer (reference quantizer.py:370-435, clustering.py:89-302) ----
+ * Sensitivity-weighted exact 1-D k-means seed (2^n_min clusters per row, by
+ * dynamic programming) and one exact weighted 2-means split per extra bit up to
+ * n_max; bit-exact with the reference's float64 arithmetic.  All pointers are
+ * device memory:
+ *   weights, sens : [rows][n] float64 (sens already coerced: finite, >= 0, every
+ *                   row sum > 0 -- quantizer.py:195-212)
+ *   order         : [rows][n] int64, the STABLE ascending argsort of each row
+ *   codes         : [rows][n] uint8 parent (n_max-bit) codes
+ *   tables        : the fp16 centroid tables for k = n_min..n_max concatenated,
+ *                   [rows][2^k] each
+ *   sse           : [n_max-n_min+1][rows] float64 weighted SSE per bit-width
+ *   level_codes   : NULL or [n_max-n_min+1][rows][n] uint8 codes at every k
+ *   workspace     : >= apb_quant_workspace(rows, n, n_min, n_max) bytes,
+ *                   16-byte aligned */
+int64_t apb_quant_workspace(int rows, int n, int n_min, int n_max);
+int apb_quant_build(const double* weights, const double* sens, const int64_t* order, int rows, int n, int n_min,
+                    int n_max, uint8_t* codes, uint16_t* tables, double* sse, uint8_t* level_codes,
+                    void* workspace, int64_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -59,6 +59,8 @@ SIGNATURES = {
     "apb_rms_residual": ([_P, _P, _P, _P, _I64, ctypes.c_float, _P], _I),
     "apb_rope_cache": ([_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I64, _P], _I),
     "apb_silu_mul": ([_P, _P, _P, _I64, _P], _I),
+    "apb_quant_workspace": ([_I, _I, _I, _I], _I64),
+    "apb_quant_build": ([_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I64, _P], _I),
     "apb_attention_decode_workspace": ([_I, _I, _I64], _I64),
     "apb_attention_decode": ([_P, _P, _P, _P, _P, _P, _P, _I, _I, _I64, _I, ctypes.c_float, _P, _I64, _P, _P, _P,
                               _P], _I),

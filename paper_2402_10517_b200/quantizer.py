@@ -1,0 +1,131 @@
+"""Any-precision quantizer on the GPU.
+
+Same entry point, argument meaning, validation order and messages as the
+reference's ``build_any_precision`` (quantizer.py:370-435, with
+``_coerce_sensitivity`` :195-212): every output channel is clustered into
+2^n_min groups by exact sensitivity-weighted 1-D k-means (dynamic programming,
+clustering.py:89-197), then each bit up to n_max splits every cluster by exact
+weighted 2-means (clustering.py:252-302).  The result is bit-identical to the
+reference: same codes, same fp16 tables, same float64 per-channel SSE.
+
+B200 path: the stable per-row argsort runs on the device (``torch.sort(...,
+stable=True)`` -- a library primitive, like cuBLAS elsewhere), everything else
+is csrc/apb_quant.cu through the C-ABI (``apb_quant_build``): one CTA per
+channel for the DP and for every bit level.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import logging
+
+import numpy as np
+
+from . import _device as dev
+from .errors import ParameterError, ShapeError
+from .layer import MAX_BITS, MIN_BITS, AnyPrecisionLayer
+
+log = logging.getLogger(__name__)
+
+# workspace budget per launch block (the DP keeps (2^n_min - 2) x n argmin rows
+# plus ~7 float64 rows per channel)
+_WORKSPACE_BUDGET = 4 << 30
+
+
+def _to_device_f64(torch, a):
+    if dev.is_tensor(a):
+        return a.to(device="cuda", dtype=torch.float64)
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))).cuda()
+
+
+def _coerce_sensitivity(torch, w, sens):
+    """quantizer.py:195-212 on the device: finite weights, sensitivity shape,
+    finite and non-negative values, zero-sum rows -> uniform (logged)."""
+    if not bool(torch.isfinite(w).all()):
+        raise ParameterError("weights must be finite")
+    if sens is None:
+        return torch.ones_like(w)
+    values = sens if dev.is_tensor(sens) or isinstance(sens, np.ndarray) else getattr(sens, "values", sens)
+    s = _to_device_f64(torch, values)
+    if tuple(s.shape) != tuple(w.shape):
+        raise ShapeError(f"sensitivity shape {tuple(s.shape)} != weights shape {tuple(w.shape)}")
+    if not bool(torch.isfinite(s).all()):
+        raise ParameterError("sensitivities must be finite")
+    if bool((s < 0).any()):
+        raise ParameterError("sensitivity values must be non-negative")
+    dead = s.sum(dim=1) <= 0
+    if bool(dead.any()):
+        idx = torch.nonzero(dead).view(-1)
+        log.warning("zero-sensitivity channel(s) %s: falling back to uniform weights", idx[:8].tolist())
+        s = s.clone()
+        s[dead] = 1.0
+    return s.contiguous()
+
+
+def build_any_precision(weights, sens, n_min: int, n_max: int, *, record_levels: bool = False,
+                        row_block: int | None = None, threads: int = 1, as_numpy: bool = True):
+    """Seed at n_min, upscale one bit at a time to n_max (quantizer.py:370-435).
+
+    ``weights`` / ``sens``: (out_channels, in_features) numpy arrays or torch
+    tensors (any float dtype; computed in float64 like the reference).  ``sens``
+    may be None (uniform), an array or a SensitivityMap-like object with
+    ``.values``.  ``row_block`` bounds the channels per device pass (default:
+    as many as a 4 GB workspace holds); ``threads`` is accepted for signature
+    compatibility.  Returns an ``AnyPrecisionLayer`` with host numpy fields
+    (``as_numpy=False``: device tensors), including ``channel_sse`` and, with
+    ``record_levels``, ``level_codes``.
+    """
+    torch = dev.require_cuda()
+    from ._lib import check, load
+
+    w = _to_device_f64(torch, weights)
+    if w.dim() != 2 or w.numel() == 0:
+        raise ShapeError("weight matrix must be a non-empty 2-D array")
+    if not MIN_BITS <= n_min <= n_max <= MAX_BITS:
+        raise ParameterError(f"bit range [{n_min}, {n_max}] outside [{MIN_BITS}, {MAX_BITS}]")
+    s = _coerce_sensitivity(torch, w.contiguous(), sens)
+    w = w.contiguous()
+    rows, n = w.shape
+    if n >= 1 << 31:
+        raise ShapeError("in_features too large")
+
+    lib = load()
+    per_row = lib.apb_quant_workspace(1, n, n_min, n_max)
+    block = max(1, min(rows, _WORKSPACE_BUDGET // max(per_row, 1)))
+    if row_block is not None:
+        block = max(1, min(block, int(row_block)))
+    levels = n_max - n_min + 1
+    codes = torch.empty(rows, n, dtype=torch.uint8, device="cuda")
+    tables = {k: torch.empty(rows, 1 << k, dtype=torch.float16, device="cuda") for k in range(n_min, n_max + 1)}
+    sse = torch.empty(levels, rows, dtype=torch.float64, device="cuda")
+    lvl = torch.empty(levels, rows, n, dtype=torch.uint8, device="cuda") if record_levels else None
+    ws = torch.empty(lib.apb_quant_workspace(block, n, n_min, n_max), dtype=torch.uint8, device="cuda")
+    st, P = dev.stream_ptr(), dev.ptr
+    for lo in range(0, rows, block):
+        hi = min(rows, lo + block)
+        nb = hi - lo
+        wb, sb = w[lo:hi], s[lo:hi]
+        # stable ascending argsort; -0.0 and +0.0 compare equal as in numpy
+        order = torch.sort(wb + 0.0, dim=1, stable=True).indices.contiguous()
+        tb = torch.empty(sum(nb << k for k in range(n_min, n_max + 1)), dtype=torch.float16, device="cuda")
+        sseb = torch.empty(levels, nb, dtype=torch.float64, device="cuda")
+        lvlb = torch.empty(levels, nb, n, dtype=torch.uint8, device="cuda") if record_levels else None
+        check(lib.apb_quant_build(P(wb), P(sb), P(order), nb, n, n_min, n_max, P(codes[lo:hi]), P(tb), P(sseb),
+                                  P(lvlb) if lvlb is not None else None, P(ws), ws.numel(), st),
+              "apb_quant_build")
+        off = 0
+        for k in range(n_min, n_max + 1):
+            tables[k][lo:hi] = tb[off:off + (nb << k)].view(nb, 1 << k)
+            off += nb << k
+        sse[:, lo:hi] = sseb
+        if record_levels:
+            lvl[:, lo:hi] = lvlb
+    conv = (lambda t: t.cpu().numpy()) if as_numpy else (lambda t: t)
+    layer = AnyPrecisionLayer(
+        n_min=n_min, n_max=n_max, codes=conv(codes),
+        centroid_tables={k: conv(t) for k, t in tables.items()},
+        shape=(rows, n),
+        channel_sse={k: conv(sse[k - n_min]) for k in range(n_min, n_max + 1)},
+    )
+    if record_levels:
+        layer.level_codes = {k: conv(lvl[k - n_min]) for k in range(n_min, n_max + 1)}
+    return layer

@@ -1,0 +1,77 @@
+"""Golden quantizer fixtures from the REFERENCE implementation
+(quantizer.build_any_precision of anyprec 0.1.0, imported read-only from
+/root/reference/pkg/src in the build container).
+
+    python tests/golden/make_quant_golden.py
+
+Writes quant_golden.npz next to this script: per case the inputs (weights,
+sensitivities or none) and the reference's outputs (parent codes, fp16 tables
+for every k, float64 channel_sse for every k, level codes).  The cases cover
+random rows with zero-sensitivity entries and a dead (all-zero) row,
+low-distinct rows (k_eff < 2^n_min, padded tables, unsplittable clusters),
+duplicates, -0.0 / +0.0 ties, n_min = 2, and a row wider than 8192 (deep
+pairwise-summation tree).  Nothing at test or bench time reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def cases():
+    rng = np.random.default_rng(2402)
+    # random rows, random sensitivities with exact zeros, one dead row
+    w = rng.standard_normal((12, 700))
+    s = rng.random((12, 700))
+    s[rng.random((12, 700)) < 0.1] = 0.0
+    s[3] = 0.0
+    yield "rand_12x700_3_8", w, s, 3, 8
+    # low-distinct rows: row i has i+1 distinct values (1..10), uniform sensitivity
+    w = np.stack([rng.choice(rng.standard_normal(i + 1), size=300) for i in range(10)])
+    yield "lowdistinct_10x300_3_6", w, None, 3, 6
+    # n_min = 2, odd width above one tile
+    w = rng.standard_normal((6, 1030)) * rng.uniform(0.01, 3.0, (6, 1))
+    s = rng.random((6, 1030)) ** 4
+    yield "nmin2_6x1030_2_5", w, s, 2, 5
+    # signed zeros, heavy ties, integer-valued weights
+    w = rng.integers(-3, 4, (5, 257)).astype(np.float64)
+    w[w == 0] = np.where(rng.random(int((w == 0).sum())) < 0.5, -0.0, 0.0)
+    s = rng.integers(0, 3, (5, 257)).astype(np.float64)
+    yield "ties_5x257_2_8", w, s, 2, 8
+    # a row wider than 8192: deeper split tree for the SSE / mean reductions
+    w = rng.standard_normal((2, 9000))
+    s = rng.random((2, 9000))
+    yield "wide_2x9000_3_5", w, s, 3, 5
+
+
+def main():
+    sys.path.insert(0, REF_SRC)
+    from anyprec.quantizer import build_any_precision  # noqa: E402
+
+    out = {}
+    names = []
+    for name, w, s, n_min, n_max in cases():
+        layer = build_any_precision(w, s, n_min, n_max, record_levels=True)
+        names.append(name)
+        out[f"{name}/weights"] = w
+        if s is not None:
+            out[f"{name}/sens"] = s
+        out[f"{name}/bits"] = np.array([n_min, n_max])
+        out[f"{name}/codes"] = layer.codes
+        for k in range(n_min, n_max + 1):
+            out[f"{name}/table{k}"] = layer.centroid_tables[k]
+            out[f"{name}/sse{k}"] = layer.channel_sse[k]
+            out[f"{name}/level{k}"] = layer.level_codes[k]
+    out["cases"] = np.array(names)
+    np.savez_compressed(os.path.join(OUT, "quant_golden.npz"), **out)
+    print("wrote", len(names), "cases")
+
+
+if __name__ == "__main__":
+    main()

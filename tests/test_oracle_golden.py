@@ -171,3 +171,19 @@ def test_random_layer_generator_reproduces_reference(eg):
     assert np.array_equal(codes, eg["L16x2000/codes"])
     for k in range(2, 9):
         assert np.array_equal(tables[k], eg[f"L16x2000/table{k}"])
+
+
+def test_quant_golden_fixture_is_consistent():
+    """The reference-made quantizer fixture: level codes are bit prefixes of
+    the parent codes and every table row is ascending (quantizer.py:4-7)."""
+    import os
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "quant_golden.npz"))
+    for name in z["cases"]:
+        name = str(name)
+        n_min, n_max = (int(v) for v in z[f"{name}/bits"])
+        codes = z[f"{name}/codes"]
+        for k in range(n_min, n_max + 1):
+            np.testing.assert_array_equal(z[f"{name}/level{k}"], codes >> (n_max - k))
+            t = z[f"{name}/table{k}"].astype(np.float64)
+            assert (np.diff(t, axis=1) >= 0).all()

@@ -1,0 +1,104 @@
+"""GPU quantizer (csrc/apb_quant.cu) against the REFERENCE's build_any_precision
+outputs (tests/golden/quant_golden.npz, made by make_quant_golden.py): codes,
+fp16 tables and float64 channel SSE must be bit-identical."""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "quant_golden.npz")
+
+
+def _cases():
+    with np.load(GOLDEN) as z:
+        return [str(c) for c in z["cases"]]
+
+
+@pytest.mark.parametrize("name", _cases())
+def test_quantizer_bit_exact_vs_reference(name):
+    from paper_2402_10517_b200.quantizer import build_any_precision
+
+    z = np.load(GOLDEN)
+    w = z[f"{name}/weights"]
+    s = z[f"{name}/sens"] if f"{name}/sens" in z else None
+    n_min, n_max = (int(v) for v in z[f"{name}/bits"])
+    layer = build_any_precision(w, s, n_min, n_max, record_levels=True)
+    assert layer.codes.dtype == np.uint8
+    np.testing.assert_array_equal(layer.codes, z[f"{name}/codes"])
+    for k in range(n_min, n_max + 1):
+        np.testing.assert_array_equal(layer.level_codes[k], z[f"{name}/level{k}"], err_msg=f"level codes k={k}")
+        np.testing.assert_array_equal(layer.centroid_tables[k].view(np.uint16),
+                                      z[f"{name}/table{k}"].view(np.uint16), err_msg=f"table k={k}")
+        np.testing.assert_array_equal(layer.channel_sse[k].view(np.uint64), z[f"{name}/sse{k}"].view(np.uint64),
+                                      err_msg=f"sse k={k}")
+
+
+def test_quantizer_row_blocks_and_torch_inputs_agree():
+    """Splitting the channels over several device passes (row_block) and
+    passing torch tensors give the same bits as one pass over numpy."""
+    import torch
+
+    from paper_2402_10517_b200.quantizer import build_any_precision
+
+    rng = np.random.default_rng(5)
+    w = rng.standard_normal((37, 2048))
+    s = rng.random((37, 2048))
+    a = build_any_precision(w, s, 3, 6)
+    b = build_any_precision(torch.from_numpy(w).cuda(), torch.from_numpy(s).cuda(), 3, 6, row_block=8)
+    np.testing.assert_array_equal(a.codes, b.codes)
+    for k in range(3, 7):
+        np.testing.assert_array_equal(a.centroid_tables[k].view(np.uint16), b.centroid_tables[k].view(np.uint16))
+        np.testing.assert_array_equal(a.channel_sse[k], b.channel_sse[k])
+
+
+def test_quantizer_full_layer_properties():
+    """Llama-2-7B q_proj-sized layer (4096 x 4096): prefix property of the codes
+    (the k-bit code is the top k bits of the parent code), ascending tables,
+    SSE never larger after a split (before fp16 rounding effects), and the
+    layer serves through the GEMV."""
+    import torch
+
+    from paper_2402_10517_b200 import engine
+    from paper_2402_10517_b200.quantizer import build_any_precision
+
+    g = torch.Generator(device="cuda").manual_seed(0)
+    w = torch.randn(4096, 4096, device="cuda", dtype=torch.float64, generator=g) * 0.02
+    s = torch.rand(4096, 4096, device="cuda", dtype=torch.float64, generator=g)
+    layer = build_any_precision(w, s, 3, 8, record_levels=True, as_numpy=False)
+    for k in range(3, 9):
+        assert torch.equal(layer.level_codes[k], layer.codes >> (8 - k)), k
+        t = layer.centroid_tables[k].float()
+        assert bool((t[:, 1:] >= t[:, :-1]).all()), k
+    sse = torch.stack([layer.channel_sse[k] for k in range(3, 9)])
+    assert bool((sse[1:] <= sse[:-1] * (1 + 1e-3) + 1e-9).all())
+    prep = engine.prepare(layer)
+    x = torch.randn(4096, device="cuda", generator=g).half()
+    for k in (3, 8):
+        y = engine.gemv(prep, x, engine.GemvConfig(bit_width=k))
+        ref = engine.dequantize(prep, k).float() @ x.float()
+        err = float((y.float() - ref).norm() / ref.norm())
+        assert err < 1e-2, (k, err)
+
+
+def test_quantizer_validation_matches_reference():
+    from paper_2402_10517_b200.errors import ParameterError, ShapeError
+    from paper_2402_10517_b200.quantizer import build_any_precision
+
+    w = np.ones((4, 16))
+    with pytest.raises(ShapeError):
+        build_any_precision(np.ones(16), None, 3, 4)
+    with pytest.raises(ParameterError):
+        build_any_precision(w, None, 1, 4)
+    with pytest.raises(ParameterError):
+        build_any_precision(w, None, 5, 4)
+    bad = w.copy()
+    bad[0, 0] = np.nan
+    with pytest.raises(ParameterError, match="weights must be finite"):
+        build_any_precision(bad, None, 3, 4)
+    with pytest.raises(ShapeError):
+        build_any_precision(w, np.ones((4, 15)), 3, 4)
+    with pytest.raises(ParameterError, match="non-negative"):
+        build_any_precision(w, -np.ones((4, 16)), 3, 4)
