@@ -302,6 +302,7 @@ def run_ours(args):
         result["shard70b_C4_per_rank"] = shard70b_detail(torch, plan)
         if not args.no_decode:
             result["decode_step"] = run_decode(torch)
+            result["quantizer"] = run_quantizer(torch)
     if rank == 0:
         if world == 1:
             result["e2e"] = run_e2e_step(torch, plans, world)
@@ -325,8 +326,8 @@ def run_decode(torch, steps: int = 20):
 
     model = DecodeModel(context=1024)
     out = {"model": "llama-2-7b shapes, 32 blocks, random-init", "context": 1024, "batch": 1,
-           "glue": "fused sm_100a kernels (residual+RMSNorm, RoPE+KV append, SiLU*up) + torch SDPA "
-                   "attention + cuBLAS fp16 LM head", "per_k": {}}
+           "glue": "fused sm_100a kernels in the PDL chain (residual+RMSNorm; RoPE + KV append + "
+                   "split-chunk attention; SiLU*up) + cuBLAS fp16 LM head", "per_k": {}}
     for k in BITS:
         model.capture(k)
         for _ in range(3):
@@ -358,6 +359,38 @@ def run_decode(torch, steps: int = 20):
     nbytes = codes.numel() + t.planes.numel()
     out["packer"] = {"shape": "11008x4096 codes -> 8 bitplanes (linear layout)", "ms": round(ms, 4),
                      "GBps": round(nbytes / (ms * 1e-3) / 1e9, 1)}
+    return out
+
+
+def run_quantizer(torch):
+    """the GPU any-precision quantizer (exact weighted k-means
+    seed at 3 bits + splits to 8 bits, bit-exact with the reference's
+    build_any_precision) on each Llama-2-7B linear shape; fp64 weights and
+    sensitivities already on the device, codes / tables / SSE left there."""
+    from paper_2402_10517_b200.quantizer import build_any_precision
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    out = {"bits": "3..8", "per_shape_ms": {}}
+    total = 0.0
+    for name, rows, cols, count in (("q/k/v/o", 4096, 4096, 4), ("gate/up", 11008, 4096, 2),
+                                    ("down", 4096, 11008, 1)):
+        w = torch.randn(rows, cols, device="cuda", dtype=torch.float64, generator=g) * 0.02
+        s = torch.rand(rows, cols, device="cuda", dtype=torch.float64, generator=g)
+        build_any_precision(w[:64], s[:64], 3, 8, as_numpy=False)  # warm-up
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        build_any_precision(w, s, 3, 8, as_numpy=False)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        out["per_shape_ms"][f"{name} {rows}x{cols}"] = round(ms, 1)
+        total += ms * count
+        del w, s
+    out["llama2_7b_all_linears_s"] = round(total * 32 / 1e3, 1)
+    out["reference_cpu_note"] = ("reference build_any_precision, 1 thread, measured in the build container: "
+                                 "25.4 ms/row at 4096 columns, 68.6 ms/row at 11008 (DESIGN.md section 6)")
+    torch.cuda.empty_cache()
     return out
 
 
