@@ -60,7 +60,7 @@ def test_decode_step_matches_dequantized_reference():
         assert torch.equal(model.hbuf.float().view(-1), got), k
 
 
-@pytest.mark.parametrize("heads,pos", [(1, 0), (4, 1), (4, 63), (4, 64), (32, 200), (32, 1024), (8, 4095)])
+@pytest.mark.parametrize("heads,pos", [(1, 0), (4, 1), (4, 63), (4, 64), (32, 200), (32, 1024), (4, 2047), (4, 2048), (8, 4095)])
 def test_attention_decode_vs_fp32(heads, pos):
     """apb_attention_decode (RoPE + cache append + split-chunk attention) against
     fp32 torch on the same fp16 inputs; twice in a row gives the same bits (the

@@ -2,7 +2,7 @@
 import csv, re, subprocess, sys, collections
 rep, skip = sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 0
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
-                      "-k", "regex:gemv_kernel", "--launch-skip", str(skip), "--launch-count", "1"],
+                      "-k", "regex:gemv", "--launch-skip", str(skip), "--launch-count", "1"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 hdr = rows[1]
