@@ -164,6 +164,26 @@ def decode_plans(plan_mod, copies, pdl: bool):
     return plans
 
 
+def fused_plans(torch, copies):
+    """The decode launch pattern with the all-gather fused into every GEMV
+    (dist.ShardedGemvPlan): one IPC-mapped output block per launch."""
+    from paper_2402_10517_b200 import dist as pdist
+
+    out, i = [], 0
+    for k in BITS:
+        for grp in GROUPS:
+            c = copies[i % len(copies)]
+            full_rows = [SHAPES[j][1] for j in grp]
+            _, nbytes = pdist.output_layout(full_rows, 1, 2)
+            g = pdist.PeerGather(nbytes)
+            sp = pdist.ShardedGemvPlan([c[j] for j in grp], full_rows, k, g, m=1, y_fp16=True,
+                                       shared_x=len(grp) > 1)
+            sp.x[0].normal_()
+            out.append(sp)
+            i += 1
+    return out
+
+
 def time_graph(torch, fn, reps: int):
     """Capture fn into a CUDA graph; return (graph, ms per replay)."""
     fn()
@@ -219,8 +239,24 @@ def run_ours(args):
 
     copies = [make_layer_set(torch, 1234 + c, rank, world) for c in range(N_COPIES)]
     plans = decode_plans(plan, copies, pdl=True)
+    # N > 1: the all-gather of the row-sharded outputs is fused into the GEMV
+    # (epilogue stores into every rank's IPC-mapped output block + arrival
+    # counters); NCCL all_gather only if that path cannot be set up here
+    fused, gather_mode = None, "none (1 GPU)"
+    if world > 1:
+        gather_mode = "nccl all_gather_into_tensor after each GEMV"
+        if not args.nccl_gather:
+            try:
+                fused = fused_plans(torch, copies)
+                gather_mode = "fused: GEMV epilogue stores over NVLink P2P + arrival counters"
+            except Exception as e:  # no P2P / IPC between these GPUs
+                print(f"[bench] fused gather unavailable ({e}); using NCCL", file=sys.stderr)
 
     def step():
+        if fused is not None:
+            for sp in fused:
+                sp.run()
+            return
         for k, grp, p in plans:
             p.run()
             if world > 1:
@@ -231,6 +267,15 @@ def run_ours(args):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    if fused is not None:  # self-check: every rank saw every arrival in time
+        bad = torch.tensor([max(sp.gather.status() for sp in fused)], device="cuda", dtype=torch.int32)
+        dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if int(bad.item()):
+            print("[bench] fused gather self-check failed; using NCCL", file=sys.stderr)
+            fused, gather_mode = None, "nccl all_gather_into_tensor after each GEMV (fused self-check failed)"
+            for _ in range(max(3, args.warmup)):
+                step()
+            torch.cuda.synchronize()
     graph = None
     try:
         if args.profile:
@@ -268,7 +313,7 @@ def run_ours(args):
     clocks = clk.summary()
     ms_per_step = ms / args.steps
     value = step_bytes() / (ms_per_step * 1e-3) / 1e9
-    launches = len(plans) * args.steps
+    launches = (2 if fused is not None else 1) * len(plans) * args.steps  # + one wait kernel per fused GEMV
     traffic, traffic_detail = measured_traffic()
 
     result = {
@@ -277,7 +322,8 @@ def run_ours(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f16 x f16 -> f32 accumulate (u8 bitplanes)", "data": "synthetic random-init",
         "config": {"workload": "llama2-7b decode layer set (configs[1])" + (
-                       "" if world == 1 else f", rows sharded over {world} GPUs + NCCL all-gather"),
+                       "" if world == 1 else f", rows sharded over {world} GPUs + all-gather of every output"),
+                   "gather": gather_mode,
                    "shapes": [f"{n}:{r}x{c}" for n, r, c in SHAPES], "bits": BITS, "batch": 1,
                    "n_max": N_MAX, "launch_groups": "qkv | o | gate+up | down per k (PDL chain)",
                    "launches_per_step": len(plans), "cuda_graph": graph is not None,
@@ -613,6 +659,8 @@ def main():
     ap.add_argument("--profile", action="store_true",
                     help="profiling run (under ncu): eager launches, skip detail/e2e/CPU legs")
     ap.add_argument("--no-decode", action="store_true", help="skip the C5 decode-step leg")
+    ap.add_argument("--nccl-gather", action="store_true",
+                    help="N > 1: all-gather with NCCL after each GEMV instead of the fused epilogue stores")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -155,6 +155,34 @@ int apb_attention_decode(const uint16_t* q, const uint16_t* k, const uint16_t* v
                          int64_t workspace_bytes, uint16_t* out, const uint16_t* next_k_cache,
                          const uint16_t* next_v_cache, void* stream);
 
+/* ---- row-sharded GEMV with the all-gather fused in ----
+ * apb_gemv_grouped_peers: apb_gemv_grouped over this rank's row slab (y[i] =
+ * this rank's rows inside its full output) that also stores every y value at
+ * the same place of each peer's output -- y_peers[i * n_peers + j] is problem
+ * i's y pointer as mapped from peer j (CUDA IPC / NVLink P2P), n_peers <= 7
+ * other ranks -- and, per CTA, adds the number of values it wrote to every
+ * rank's arrival counter (peer_flags[0..n_peers-1] the peers', then
+ * peer_flags[n_peers] this rank's own) with release semantics at system scope.
+ * k 3..8, m_x <= 8, <= 16 problems, <= 64K columns.
+ * apb_peer_wait: on the stream, wait until *arrivals has grown by per_step
+ * (the full output's values) since the previous wait (*expected tracks the
+ * target in device memory: graph-replayable); gives up after spin_limit polls
+ * and sets *status = 1.
+ * apb_peer_alloc / open / close / free: cudaMalloc'd (zeroed) region + its
+ * IPC handle (apb_peer_handle_bytes() bytes), and the peer-side mapping. */
+int apb_gemv_grouped_peers(int n_problems, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
+                           const int64_t* cols, const int64_t* padded_cols, int k, const uint16_t* const* lut,
+                           const uint16_t* const* x, int m_x, const int64_t* ldx, int x_split, void* const* y,
+                           int y_dtype, const int64_t* ldy, int n_peers, void* const* y_peers,
+                           uint32_t* const* peer_flags, int flags, void* stream);
+int apb_peer_wait(const uint32_t* arrivals, uint32_t* expected, uint32_t per_step, int* status,
+                  long long spin_limit, void* stream);
+int apb_peer_alloc(int64_t bytes, void** ptr, void* handle);
+int apb_peer_open(const void* handle, void** ptr);
+int apb_peer_close(void* ptr);
+int apb_peer_free(void* ptr);
+int apb_peer_handle_bytes(void);
+
 /* ---- offline quantizer (reference quantizer.py:370-435, clustering.py:89-302) ----
  * Sensitivity-weighted exact 1-D k-means seed (2^n_min clusters per row, by
  * dynamic programming) and one exact weighted 2-means split per extra bit up to

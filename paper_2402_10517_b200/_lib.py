@@ -59,6 +59,16 @@ SIGNATURES = {
     "apb_rms_residual": ([_P, _P, _P, _P, _I64, ctypes.c_float, _P], _I),
     "apb_rope_cache": ([_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I64, _P], _I),
     "apb_silu_mul": ([_P, _P, _P, _I64, _P], _I),
+    "apb_gemv_grouped_peers": (
+        [_I, _PP, _PI, _PI64, _PI64, _PI64, _I, _PP, _PP, _I, _PI64, _I, _PP, _I, _PI64, _I, _PP, _PP, _I, _P],
+        _I,
+    ),
+    "apb_peer_wait": ([_P, _P, ctypes.c_uint32, _P, ctypes.c_longlong, _P], _I),
+    "apb_peer_alloc": ([_I64, _P, _P], _I),
+    "apb_peer_open": ([_P, _P], _I),
+    "apb_peer_close": ([_P], _I),
+    "apb_peer_free": ([_P], _I),
+    "apb_peer_handle_bytes": ([], _I),
     "apb_quant_workspace": ([_I, _I, _I, _I], _I64),
     "apb_quant_build": ([_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I64, _P], _I),
     "apb_attention_decode_workspace": ([_I, _I, _I64], _I64),

@@ -1107,7 +1107,8 @@ static int gemv_launch_chunk(int n, const uint8_t* const* planes, const int64_t*
 extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
                              const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
                              const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split,
-                             void* const* y, int y_dtype, const int64_t* ldy, int64_t y_off, int flags, void* stream);
+                             void* const* y, int y_dtype, const int64_t* ldy, int64_t y_off, int flags, void* stream, int n_peers,
+                             void* const* y_peers, uint32_t* const* peer_flags);
 
 extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, const int* n_max,
                                 const int64_t* rows, const int64_t* cols,
@@ -1132,7 +1133,7 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
     cudaStream_t s = (cudaStream_t)stream;
     if (m_x <= 8 && n_problems <= 16) {  // TMA-fed kernel (apb_gemv7.cu)
         const int rc = apb7_try_gemv(n_problems, planes, n_max, rows, cols, padded_cols, k, lut, x, m_x, ldx, 0,
-                                     x_split, y, y_dtype, ldy, 0, flags, stream);
+                                     x_split, y, y_dtype, ldy, 0, flags, stream, 0, nullptr, nullptr);
         if (rc != -1) return rc;
     }
     // batch columns per launch: 32 fp16 activation rows (4 mma column groups)
@@ -1148,6 +1149,42 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
         }
     }
     return APB_OK;
+}
+
+// Row-sharded GEMV with the all-gather fused into the epilogue:
+// the grouped GEMV of this rank's row slab, every y value also stored into the
+// same place of each peer's output (y_peers[i * n_peers + j]: problem i's y as
+// mapped from peer j, e.g. through CUDA IPC), and each CTA adding the number of
+// values it wrote to every rank's arrival counter (peer_flags[0..n_peers-1] the
+// peers', peer_flags[n_peers] this rank's own).  apb_peer_wait completes it.
+extern "C" int apb_gemv_grouped_peers(int n_problems, const uint8_t* const* planes, const int* n_max,
+                                      const int64_t* rows, const int64_t* cols, const int64_t* padded_cols, int k,
+                                      const uint16_t* const* lut, const uint16_t* const* x, int m_x,
+                                      const int64_t* ldx, int x_split, void* const* y, int y_dtype,
+                                      const int64_t* ldy, int n_peers, void* const* y_peers,
+                                      uint32_t* const* peer_flags, int flags, void* stream) {
+    if (n_problems < 1) return APB_ERR_SHAPE;
+    if (k < 3 || k > 8) return APB_ERR_PARAM;  // the TMA kernel's range
+    if (y_dtype != APB_DTYPE_F32 && y_dtype != APB_DTYPE_F16) return APB_ERR_PARAM;
+    if (m_x < 1 || m_x > 8 || n_problems > 16 || (x_split && (m_x & 1))) return APB_ERR_SHAPE;
+    if (n_peers < 0 || n_peers > 7 || (n_peers > 0 && !y_peers) || !peer_flags) return APB_ERR_PARAM;
+    for (int j = 0; j <= n_peers; ++j)
+        if (!peer_flags[j] || ((uintptr_t)peer_flags[j] & 3)) return APB_ERR_PARAM;
+    for (int i = 0; i < n_problems; ++i) {
+        if (rows[i] <= 0 || cols[i] <= 0) return APB_ERR_SHAPE;
+        if (padded_cols[i] != apb_pad_columns(cols[i])) return APB_ERR_SHAPE;
+        if (k > n_max[i] || n_max[i] > 8) return APB_ERR_PARAM;
+        if (ldx[i] < cols[i] || (ldx[i] % 8) != 0) return APB_ERR_PARAM;
+        if (!planes[i] || !lut[i] || !x[i] || !y[i]) return APB_ERR_PARAM;
+        if (((uintptr_t)x[i] & 15) != 0 || ((uintptr_t)planes[i] & 15) != 0) return APB_ERR_PARAM;
+        if (((uintptr_t)lut[i] & 15) != 0) return APB_ERR_PARAM;
+        if (ldy[i] < rows[i]) return APB_ERR_SHAPE;
+        for (int j = 0; j < n_peers; ++j)
+            if (!y_peers[(size_t)i * n_peers + j]) return APB_ERR_PARAM;
+    }
+    const int rc = apb7_try_gemv(n_problems, planes, n_max, rows, cols, padded_cols, k, lut, x, m_x, ldx, 0,
+                                 x_split, y, y_dtype, ldy, 0, flags, stream, n_peers, y_peers, peer_flags);
+    return rc == -1 ? APB_ERR_PARAM : rc;  // e.g. more than 64K columns: not on the fused path
 }
 
 #ifdef APB_TIMELINE

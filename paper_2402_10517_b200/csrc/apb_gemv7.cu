@@ -47,6 +47,7 @@ using apb::prmt;
 
 constexpr int kRows = 16;      // rows per item
 constexpr int kMaxProb = 16;   // problems per grouped launch
+constexpr int kMaxPeers = 8;   // fused all-gather: ranks of one NVSwitch node
 constexpr int kSmemBase = 1024;  // sm_100 reserves the first 1 KB of the shared window
 constexpr int kMaxCols = 64 * 1024;  // padded columns per layer on this path
 
@@ -93,6 +94,12 @@ struct alignas(64) Launch7 {
     int64_t xs_bytes;  // one activation buffer
     int x_bufs;        // 1 when every problem shares one x, else 2
     int tl_launch;     // APB_TIMELINE builds: launch index
+    // fused all-gather of row-sharded outputs: every y value is also stored at
+    // the same offset of each peer's output (P2P over NVLink), and each CTA then
+    // adds the number of y values it wrote to every peer's arrival counter
+    int n_peers;
+    uint8_t* y_peer[kMaxProb][kMaxPeers];
+    uint32_t* peer_flag[kMaxPeers + 1];  // the n_peers others, then this rank's own
 };
 
 template <int K, int NB = 1, int CPS = 1>
@@ -529,6 +536,7 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
     if (warp == WC + 1) {
         // ========================= service: tables, x, y =========================
         const int g = lane >> 2, q = lane & 3, rho = 2 * g + (q >> 1);
+        uint32_t y_written = 0;  // y values this lane stored (fused all-gather accounting)
         auto reduce = [&](int item, int pi, int slot) {
             const Prob7& P = L.prob[pi];
             const int m_out = L.x_split ? (L.m_x >> 1) : L.m_x;
@@ -551,10 +559,16 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
 #pragma unroll
                     for (int w = 0; w < WC; ++w) sum += r[(w * 2 * NB + m) * kRows + rl];
                 }
-                if (L.y_f16)
-                    reinterpret_cast<__half*>(P.y)[(int64_t)m * P.ldy + row] = __float2half_rn(sum);
-                else
-                    reinterpret_cast<float*>(P.y)[(int64_t)m * P.ldy + row] = sum;
+                const int64_t off = (int64_t)m * P.ldy + row;
+                if (L.y_f16) {
+                    const __half hv = __float2half_rn(sum);
+                    reinterpret_cast<__half*>(P.y)[off] = hv;
+                    for (int j = 0; j < L.n_peers; ++j) reinterpret_cast<__half*>(L.y_peer[pi][j])[off] = hv;
+                } else {
+                    reinterpret_cast<float*>(P.y)[off] = sum;
+                    for (int j = 0; j < L.n_peers; ++j) reinterpret_cast<float*>(L.y_peer[pi][j])[off] = sum;
+                }
+                ++y_written;
             }
         };
 
@@ -614,6 +628,17 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                 }
                 if (jl == 0 && lane == 0) APB_TL(1);
             }
+        }
+        if (L.n_peers >= 0) {
+            // publish: every lane's local + peer stores visible system-wide, then
+            // one release-add per rank of the values this CTA wrote
+            __threadfence_system();
+            uint32_t tot = y_written;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+            __syncwarp();
+            if (lane <= L.n_peers && tot > 0)  // peers' counters, then this rank's own
+                asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(L.peer_flag[lane]), "r"(tot) : "memory");
         }
         if (lane == 0) APB_TL(5);
         return;
@@ -1038,7 +1063,8 @@ extern "C" void apb7_timeline_reset(void) { g_tl_host_launch = 0; }
 extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
                              const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
                              const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split,
-                             void* const* y, int y_dtype, const int64_t* ldy, int64_t y_off, int flags, void* stream) {
+                             void* const* y, int y_dtype, const int64_t* ldy, int64_t y_off, int flags, void* stream,
+                             int n_peers, void* const* y_peers, uint32_t* const* peer_flags) {
     using namespace apb7;
     static const bool disabled = [] {
         const char* e = std::getenv("APB_GEMV_V7");
@@ -1046,7 +1072,7 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     }();
     // batch rows: <= 2 row-copy mapping (x in smem), 3..8 batch-in-N mapping
     // (measured faster than the two-batch-pair row-copy path from 3 rows up)
-    if (disabled || k < 3 || k > 8 || m_x > 8 || n > kMaxProb) return -1;
+    if (disabled || k < 3 || k > 8 || m_x > 8 || n > kMaxProb || n_peers > kMaxPeers - 1) return -1;
     for (int i = 0; i < n; ++i)
         if (padded[i] > kMaxCols) return -1;
     static thread_local Launch7 L;  // ~5 KB: kept off the stack
@@ -1065,6 +1091,8 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
         if (!make_lut_map(&L.tm_lut[i], lut[i], k, rows[i])) return -1;
         P.x = x[i] + x_off * ldx[i];
         P.y = reinterpret_cast<uint8_t*>(y[i]) + y_off * ldy[i] * esz;
+        for (int j = 0; j < n_peers; ++j)  // the same region of every peer's output
+            L.y_peer[i][j] = reinterpret_cast<uint8_t*>(y_peers[(size_t)i * n_peers + j]) + y_off * ldy[i] * esz;
         P.rows = rows[i];
         P.cols = cols[i];
         P.ldx = ldx[i];
@@ -1092,6 +1120,9 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
         if (L.prob[i].xid == i) ++n_xid;
     }
     L.x_bufs = n_xid == 1 ? 1 : 2;
+    L.n_peers = peer_flags ? n_peers : -1;  // -1: no fused gather at all
+    if (peer_flags)
+        for (int j = 0; j <= n_peers; ++j) L.peer_flag[j] = peer_flags[j];
 #ifdef APB_TIMELINE
     L.tl_launch = g_tl_host_launch++;
 #endif

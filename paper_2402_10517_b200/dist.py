@@ -9,11 +9,15 @@ its slice with the local GEMV kernel and all-gathers the fp32 (or fp16) y slices
 over NVLink (NCCL).  x is replicated.
 
 The only exchange step is the all-gather; uneven shards are padded to the
-largest shard and trimmed after the collective.
+largest shard and trimmed after the collective (``gather_rows``, NCCL), or --
+the B200 path -- fused into the GEMV itself: ``ShardedGemvPlan`` stores every
+output value straight into every rank's output block over NVLink and counts
+the arrivals (``PeerGather`` holds the IPC-mapped blocks).
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 from . import _device as dev
@@ -99,3 +103,199 @@ class RowShardedLayer:
         torch = dev.torch()
         y = gemm(self.local, x if dev.is_tensor(x) else torch.as_tensor(x).cuda(), cfg, report)
         return gather_rows(y, self.rows, self.group)
+
+
+# ---------------------------------------------------------------------------
+# Fused all-gather: the GEMV epilogue stores every output value into every
+# rank's output block over NVLink (apb_gemv_grouped_peers), then a one-thread
+# wait kernel (apb_peer_wait) completes the step.  No NCCL on the data path.
+
+_CTRL_BYTES = 64  # arrivals u32 | expected u32 | status i32 | pad
+
+
+def _align(n: int, a: int = 256) -> int:
+    return -(-n // a) * a
+
+
+def output_layout(rows_list, m: int, esz: int):
+    """Byte offsets of the full outputs [m][rows] inside a rank's block, and the
+    block size (outputs + control words).  Identical on every rank."""
+    offs, o = [], 0
+    for r in rows_list:
+        offs.append(o)
+        o += _align(m * r * esz)
+    return offs, o + _CTRL_BYTES
+
+
+def slab_pointers(bases, rank: int, offs, full_rows, m: int, esz: int, ctrl_off: int):
+    """Addresses the fused launch of ``rank`` needs, from every rank's block base
+    as mapped in this process: its own slab of each output, the same slab in
+    each peer's block (``[problem][peer]``, peers in rank order without
+    ``rank``), and the arrival counters (peers, then own)."""
+    world = len(bases)
+    peers = [r for r in range(world) if r != rank]
+    r0s = [shard_bounds(R, world, rank)[0] for R in full_rows]
+    own = [bases[rank] + o + r0 * esz for o, r0 in zip(offs, r0s)]
+    y_peers = [bases[p] + o + r0 * esz for o, r0 in zip(offs, r0s) for p in peers]
+    flags = [bases[p] + ctrl_off for p in peers] + [bases[rank] + ctrl_off]
+    return own, y_peers, flags
+
+
+class PeerGather:
+    """One symmetric block per rank (cudaMalloc + CUDA IPC handle), every peer's
+    block opened in this process; ``bases[r]`` is rank r's block as addressed
+    from here.  Control words at ``ctrl_off``: arrivals, expected, status."""
+
+    def __init__(self, nbytes: int, group=None):
+        import torch.distributed as dist
+
+        from ._lib import check, load
+
+        lib = load()
+        self._lib = lib
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.nbytes = nbytes
+        self.ctrl_off = nbytes - _CTRL_BYTES
+        hb = lib.apb_peer_handle_bytes()
+        handle = ctypes.create_string_buffer(hb)
+        ptr = ctypes.c_void_p()
+        check(lib.apb_peer_alloc(nbytes, ctypes.byref(ptr), handle), "apb_peer_alloc")
+        self._own = ptr.value
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle.raw), group=group)
+        self.bases, self._opened = [], []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                self.bases.append(self._own)
+                continue
+            p = ctypes.c_void_p()
+            check(lib.apb_peer_open(ctypes.create_string_buffer(h, hb), ctypes.byref(p)), "apb_peer_open")
+            self.bases.append(p.value)
+            self._opened.append(p.value)
+        dist.barrier(group)
+
+    @classmethod
+    def simulated(cls, nbytes: int, world: int):
+        """``world`` blocks in ONE process on one GPU, each "rank" addressing the
+        others directly -- the single-GPU test bed for the fused gather."""
+        torch = dev.require_cuda()
+        blocks = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(world)]
+        out = []
+        for r in range(world):
+            g = cls.__new__(cls)
+            g._lib, g.world, g.rank, g.nbytes = None, world, r, nbytes
+            g.ctrl_off = nbytes - _CTRL_BYTES
+            g.bases = [dev.ptr(b) for b in blocks]
+            g._own, g._opened, g._blocks = g.bases[r], [], blocks
+            out.append(g)
+        return out
+
+    def arrivals(self, rank=None) -> int:
+        return self.bases[self.rank if rank is None else rank] + self.ctrl_off
+
+    def view(self, offset: int, shape, dtype):
+        """The own block's bytes [offset, ...) as a torch tensor (no copy)."""
+        torch = dev.torch()
+        if hasattr(self, "_blocks"):
+            blk = self._blocks[self.rank]
+        else:
+            blk = _wrap_device_bytes(torch, self._own, self.nbytes)
+        n = 1
+        for d in shape:
+            n *= d
+        esz = torch.tensor([], dtype=dtype).element_size()
+        return blk[offset: offset + n * esz].view(dtype).view(*shape)
+
+    def status(self) -> int:
+        torch = dev.torch()
+        return int(self.view(self.ctrl_off + 8, (1,), torch.int32).item())
+
+    def close(self):
+        if self._lib is None:
+            return
+        for p in self._opened:
+            self._lib.apb_peer_close(p)
+        self._lib.apb_peer_free(self._own)
+        self._opened, self._lib = [], None
+
+
+def _wrap_device_bytes(torch, address: int, nbytes: int):
+    """A uint8 CUDA tensor over memory this package allocated (no ownership)."""
+    class _Cuda:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (address, False), "version": 3}
+
+    return torch.as_tensor(_Cuda(), device="cuda")
+
+
+class ShardedGemvPlan:
+    """This rank's row slab of a grouped GEMV whose outputs are all-gathered by
+    the kernel itself: ``launch_gemv()`` writes every rank's block,
+    ``launch_wait()`` blocks the stream until all ranks' slabs have landed in
+    this rank's block; ``run()`` does both.  ``y[i]`` is the full [m][rows_i]
+    output of problem i in this rank's block."""
+
+    def __init__(self, local_preps, full_rows, k: int, gather: PeerGather, m: int = 1, y_fp16: bool = True,
+                 pdl: bool = True, shared_x: bool = False, spin_limit: int = 1 << 26):
+        from ._lib import APB_DTYPE_F16, APB_DTYPE_F32, APB_FLAG_PDL, int64_array, int_array, load, ptr_array
+        from .plan import _ldx
+
+        torch = dev.require_cuda()
+        self._lib = load()
+        self.k, self.m, self.gather = k, m, gather
+        world, rank = gather.world, gather.rank
+        esz = 2 if y_fp16 else 4
+        self.y_dtype = APB_DTYPE_F16 if y_fp16 else APB_DTYPE_F32
+        self.flags = APB_FLAG_PDL if pdl else 0
+        offs, need = output_layout(full_rows, m, esz)
+        if need > gather.nbytes:
+            raise ValueError("PeerGather block too small for these outputs")
+        ts = [p.tensor for p in local_preps]
+        for t, R in zip(ts, full_rows):
+            if t.rows != shard_bounds(R, world, rank)[1] - shard_bounds(R, world, rank)[0]:
+                raise ValueError("local layer rows do not match this rank's shard")
+        if shared_x:
+            x0 = torch.zeros((m, _ldx(ts[0].cols)), dtype=torch.float16, device="cuda")
+            self.x = [x0] * len(ts)
+        else:
+            self.x = [torch.zeros((m, _ldx(t.cols)), dtype=torch.float16, device="cuda") for t in ts]
+        ydt = torch.float16 if y_fp16 else torch.float32
+        self.y = [gather.view(o, (m, R), ydt) for o, R in zip(offs, full_rows)]
+        self.per_step = sum(m * R for R in full_rows)
+        own, y_peers, flagp = slab_pointers(gather.bases, rank, offs, full_rows, m, esz, gather.ctrl_off)
+        self._n = len(ts)
+        self._n_peers = world - 1
+        self._planes = ptr_array([dev.ptr(t.planes) for t in ts])
+        self._nmax = int_array([t.n_max for t in ts])
+        self._rows = int64_array([t.rows for t in ts])
+        self._cols = int64_array([t.cols for t in ts])
+        self._padded = int64_array([t.padded_cols for t in ts])
+        self._lut = ptr_array([dev.ptr(p.tables16[k]) for p in local_preps])
+        self._xp = ptr_array([dev.ptr(x) for x in self.x])
+        self._ldx = int64_array([x.shape[1] for x in self.x])
+        self._yp = ptr_array(own)
+        self._ldy = int64_array(list(full_rows))
+        self._ypeers = ptr_array(y_peers or [0])
+        self._flagp = ptr_array(flagp)
+        ctrl = gather.bases[rank] + gather.ctrl_off
+        self._arr, self._exp, self._status = ctrl, ctrl + 4, ctrl + 8
+        self._spin = spin_limit
+
+    def launch_gemv(self):
+        from ._lib import check
+
+        P = lambda a: ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))  # noqa: E731
+        check(self._lib.apb_gemv_grouped_peers(
+            self._n, P(self._planes), self._nmax, self._rows, self._cols, self._padded, self.k, P(self._lut),
+            P(self._xp), self.m, self._ldx, 0, P(self._yp), self.y_dtype, self._ldy, self._n_peers,
+            P(self._ypeers), P(self._flagp), self.flags, dev.stream_ptr()), "apb_gemv_grouped_peers")
+
+    def launch_wait(self):
+        from ._lib import check
+
+        check(self._lib.apb_peer_wait(self._arr, self._exp, self.per_step, self._status, self._spin,
+                                      dev.stream_ptr()), "apb_peer_wait")
+
+    def run(self):
+        self.launch_gemv()
+        self.launch_wait()

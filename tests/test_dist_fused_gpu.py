@@ -1,0 +1,140 @@
+"""Fused GEMV + all-gather (dist.ShardedGemvPlan over apb_gemv_grouped_peers /
+apb_peer_wait) on ONE GPU: P simulated ranks, each with its own output block,
+address each other's blocks directly -- the same stores and arrival counters
+the IPC-mapped multi-GPU path uses.  Every rank must end each step holding the
+complete output, bit-identical to the concatenation of the per-shard outputs of
+the plain launch, and the bounded wait must time out (not hang) when a peer's
+arrivals are missing."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as ora
+
+pytestmark = pytest.mark.gpu
+
+
+def _layer(seed, rows, cols):
+    from paper_2402_10517_b200 import AnyPrecisionLayer
+
+    codes, tables = ora.random_layer_arrays(np.random.default_rng(seed), rows, cols, 3, 8)
+    return AnyPrecisionLayer(n_min=3, n_max=8, codes=codes, centroid_tables=tables, shape=(rows, cols))
+
+
+@pytest.mark.parametrize("world,k,m,fp16", [(2, 3, 1, True), (3, 5, 1, False), (4, 8, 4, True), (2, 4, 2, False)])
+def test_fused_allgather_simulated_ranks(world, k, m, fp16):
+    import torch
+
+    from paper_2402_10517_b200 import dist, engine, plan
+
+    shapes = [(1000, 3000), (777, 3000)]
+    layers = [_layer(10 + i, r, c) for i, (r, c) in enumerate(shapes)]
+    full_rows = [r for r, _ in shapes]
+    esz = 2 if fp16 else 4
+    _, nbytes = dist.output_layout(full_rows, m, esz)
+    gathers = dist.PeerGather.simulated(nbytes, world)
+    shard_preps = [[engine.prepare(dist.shard_layer(L, world, r)) for L in layers] for r in range(world)]
+    plans = [dist.ShardedGemvPlan(shard_preps[r], full_rows, k, gathers[r], m=m, y_fp16=fp16, shared_x=True,
+                                  spin_limit=1 << 22) for r in range(world)]
+    refs = [plan.GemvPlan(shard_preps[r], k, m=m, grouped=True, shared_x=True, y_fp16=fp16) for r in range(world)]
+    g = torch.Generator(device="cuda").manual_seed(world * 10 + k)
+    for step in range(3):  # the arrival targets advance per step
+        x = torch.randn(m, 3000, device="cuda", generator=g).half()
+        for p in plans + refs:
+            p.x[0][:, :3000].copy_(x)
+        for p in plans:
+            p.launch_gemv()
+        for p in plans:
+            p.launch_wait()
+        for p in refs:
+            p.run()
+        torch.cuda.synchronize()
+        for r in range(world):
+            assert gathers[r].status() == 0, (step, r)
+        for i, R in enumerate(full_rows):
+            want = torch.cat([refs[r].y[i] for r in range(world)], dim=1)
+            for r in range(world):
+                assert torch.equal(plans[r].y[i], want.to(plans[r].y[i].dtype)), (step, r, i)
+        # and the numbers are the layer's: vs the unsharded API
+        y_full = engine.gemv(engine.prepare(layers[0]), x[0], engine.GemvConfig(bit_width=k, activations_fp16=True))
+        err = float((plans[0].y[0][0].float() - y_full.float()).norm() / y_full.float().norm())
+        assert err < (2e-3 if fp16 else 1e-5), err
+
+
+def test_fused_allgather_wait_times_out_instead_of_hanging():
+    import torch
+
+    from paper_2402_10517_b200 import dist, engine
+
+    L = _layer(3, 512, 1024)
+    _, nbytes = dist.output_layout([512], 1, 2)
+    gathers = dist.PeerGather.simulated(nbytes, 2)
+    p0 = dist.ShardedGemvPlan([engine.prepare(dist.shard_layer(L, 2, 0))], [512], 3, gathers[0], spin_limit=20000)
+    p0.run()  # rank 1 never contributes
+    torch.cuda.synchronize()
+    assert gathers[0].status() == 1
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2402_10517_b200 import dist, engine, plan
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)  # both "ranks" on the one GPU: same-device IPC
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shapes = [(1000, 2048), (300, 2048)]
+        layers = [_layer(40 + i, r, c) for i, (r, c) in enumerate(shapes)]
+        full_rows = [r for r, _ in shapes]
+        _, nbytes = dist.output_layout(full_rows, 1, 2)
+        g = dist.PeerGather(nbytes)  # cudaMalloc + IPC handle, exchanged over gloo
+        preps = [engine.prepare(dist.shard_layer(L, world, rank)) for L in layers]
+        sp = dist.ShardedGemvPlan(preps, full_rows, 4, g, shared_x=True, spin_limit=1 << 26)
+        ref = plan.GemvPlan(preps, 4, grouped=True, shared_x=True, y_fp16=True)
+        ok = True
+        for step in range(3):
+            x = torch.randn(1, 2048, generator=torch.Generator().manual_seed(step)).half().cuda()
+            sp.x[0][:, :2048].copy_(x)
+            ref.x[0][:, :2048].copy_(x)
+            sp.run()
+            ref.run()
+            torch.cuda.synchronize()
+            ok = ok and g.status() == 0
+            slabs = [None] * world
+            tdist.all_gather_object(slabs, [y.cpu() for y in ref.y])
+            for i in range(len(shapes)):
+                want = torch.cat([slabs[r][i] for r in range(world)], dim=1)
+                ok = ok and torch.equal(sp.y[i].cpu(), want)
+            tdist.barrier()
+        g.close()
+        q.put((rank, bool(ok)))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_fused_allgather_two_processes_ipc():
+    """The real multi-process path (IPC-mapped blocks, cross-process stores and
+    system-scope arrival counters), both ranks on the one GPU of the box."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(240)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    assert all(ok for _, ok in res), res
