@@ -54,6 +54,12 @@ enum { APB_DTYPE_F32 = 0, APB_DTYPE_F16 = 1 };
  * reading activations or writing outputs.  Only set it when the preceding
  * kernel does not write the planes or tables of this call. */
 enum { APB_FLAG_PDL = 1 };
+/* APB_FLAG_GLU: every problem's rows are interleaved (gate_i, up_i) pairs (rows
+ * even) and the output has rows / 2 values per batch row,
+ * y[m][i] = silu(gate_i . x_m) * (up_i . x_m), from the fp32 row sums, rounded
+ * once to y_dtype (the Llama MLP's SiLU * up fused into the gate/up GEMV).
+ * TMA kernel only (k 3..8, m_x <= 8, <= 16 problems); else APB_ERR_PARAM. */
+enum { APB_FLAG_GLU = 2 };
 
 /* Library version (major*10000 + minor*100 + patch) and status strings. */
 int apb_version(void);

@@ -33,6 +33,7 @@ APB_ERR_NCCL = 6
 APB_DTYPE_F32 = 0
 APB_DTYPE_F16 = 1
 APB_FLAG_PDL = 1
+APB_FLAG_GLU = 2
 
 # Every symbol declared in include/anyprec_b200.h, with its ctypes signature.
 _P = ctypes.c_void_p

@@ -1120,15 +1120,16 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
     if (k < 2 || k > 8) return APB_ERR_PARAM;
     if (y_dtype != APB_DTYPE_F32 && y_dtype != APB_DTYPE_F16) return APB_ERR_PARAM;
     if (m_x < 1 || (x_split && (m_x & 1))) return APB_ERR_SHAPE;
+    const bool glu = (flags & APB_FLAG_GLU) != 0;
     for (int i = 0; i < n_problems; ++i) {
-        if (rows[i] <= 0 || cols[i] <= 0) return APB_ERR_SHAPE;
+        if (rows[i] <= 0 || cols[i] <= 0 || (glu && (rows[i] & 1))) return APB_ERR_SHAPE;
         if (padded_cols[i] != apb_pad_columns(cols[i])) return APB_ERR_SHAPE;
         if (k > n_max[i] || n_max[i] > 8) return APB_ERR_PARAM;
         if (ldx[i] < cols[i] || (ldx[i] % 8) != 0) return APB_ERR_PARAM;
         if (!planes[i] || !lut[i] || !x[i] || !y[i]) return APB_ERR_PARAM;
         if (((uintptr_t)x[i] & 15) != 0 || ((uintptr_t)planes[i] & 15) != 0) return APB_ERR_PARAM;
         if (((uintptr_t)lut[i] & 15) != 0) return APB_ERR_PARAM;
-        if (ldy[i] < rows[i]) return APB_ERR_SHAPE;
+        if (ldy[i] < (glu ? rows[i] / 2 : rows[i])) return APB_ERR_SHAPE;
     }
     cudaStream_t s = (cudaStream_t)stream;
     if (m_x <= 8 && n_problems <= 16) {  // TMA-fed kernel (apb_gemv7.cu)
@@ -1136,6 +1137,7 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
                                      x_split, y, y_dtype, ldy, 0, flags, stream, 0, nullptr, nullptr);
         if (rc != -1) return rc;
     }
+    if (glu) return APB_ERR_PARAM;  // the gate/up epilogue exists on the TMA kernel only
     // batch columns per launch: 32 fp16 activation rows (4 mma column groups)
     const int chunk = 32;
     for (int p0 = 0; p0 < n_problems; p0 += kMaxGroup) {
@@ -1178,7 +1180,8 @@ extern "C" int apb_gemv_grouped_peers(int n_problems, const uint8_t* const* plan
         if (!planes[i] || !lut[i] || !x[i] || !y[i]) return APB_ERR_PARAM;
         if (((uintptr_t)x[i] & 15) != 0 || ((uintptr_t)planes[i] & 15) != 0) return APB_ERR_PARAM;
         if (((uintptr_t)lut[i] & 15) != 0) return APB_ERR_PARAM;
-        if (ldy[i] < rows[i]) return APB_ERR_SHAPE;
+        if ((flags & APB_FLAG_GLU) && (rows[i] & 1)) return APB_ERR_SHAPE;
+        if (ldy[i] < ((flags & APB_FLAG_GLU) ? rows[i] / 2 : rows[i])) return APB_ERR_SHAPE;
         for (int j = 0; j < n_peers; ++j)
             if (!y_peers[(size_t)i * n_peers + j]) return APB_ERR_PARAM;
     }

@@ -90,6 +90,7 @@ struct alignas(64) Launch7 {
     int n_prob, n_items;
     int64_t total_cost;
     int m_x, x_split, y_f16;
+    int glu;           // APB_FLAG_GLU: interleaved (gate, up) rows -> silu(gate) * up
     int n_stages;      // ring depth
     int64_t xs_bytes;  // one activation buffer
     int x_bufs;        // 1 when every problem shares one x, else 2
@@ -542,33 +543,47 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
             const int m_out = L.x_split ? (L.m_x >> 1) : L.m_x;
             const int64_t row0 = (int64_t)(item - P.item_begin) * kRows;
             const float* r = red + slot * (WC * 2 * NB * kRows);
-            for (int i = lane; i < kRows * m_out; i += 32) {
-                const int rl = i & 15, m = i >> 4;
-                const int64_t row = row0 + rl;
-                if (row >= P.rows) continue;
-                float sum;
+            auto row_sum = [&](int rl, int m) {
                 if (L.x_split) {  // batch rows (2m, 2m+1) = (hi, lo) halves of fp32 x
                     float hi = 0.f, lo = 0.f;
 #pragma unroll
                     for (int w = 0; w < WC; ++w) hi += r[(w * 2 * NB + 2 * m) * kRows + rl];
 #pragma unroll
                     for (int w = 0; w < WC; ++w) lo += r[(w * 2 * NB + 2 * m + 1) * kRows + rl];
-                    sum = hi + lo;
-                } else {
-                    sum = 0.f;
-#pragma unroll
-                    for (int w = 0; w < WC; ++w) sum += r[(w * 2 * NB + m) * kRows + rl];
+                    return hi + lo;
                 }
-                const int64_t off = (int64_t)m * P.ldy + row;
+                float sum = 0.f;
+#pragma unroll
+                for (int w = 0; w < WC; ++w) sum += r[(w * 2 * NB + m) * kRows + rl];
+                return sum;
+            };
+            auto store = [&](int m, int64_t orow, float v) {
+                const int64_t off = (int64_t)m * P.ldy + orow;
                 if (L.y_f16) {
-                    const __half hv = __float2half_rn(sum);
+                    const __half hv = __float2half_rn(v);
                     reinterpret_cast<__half*>(P.y)[off] = hv;
                     for (int j = 0; j < L.n_peers; ++j) reinterpret_cast<__half*>(L.y_peer[pi][j])[off] = hv;
                 } else {
-                    reinterpret_cast<float*>(P.y)[off] = sum;
-                    for (int j = 0; j < L.n_peers; ++j) reinterpret_cast<float*>(L.y_peer[pi][j])[off] = sum;
+                    reinterpret_cast<float*>(P.y)[off] = v;
+                    for (int j = 0; j < L.n_peers; ++j) reinterpret_cast<float*>(L.y_peer[pi][j])[off] = v;
                 }
                 ++y_written;
+            };
+            if (L.glu) {  // rows (2i, 2i+1) = (gate_i, up_i): y[i] = silu(gate_i . x) * (up_i . x)
+                for (int i = lane; i < (kRows / 2) * m_out; i += 32) {
+                    const int pr = i & 7, m = i >> 3;
+                    const int64_t row = row0 + 2 * pr;
+                    if (row >= P.rows) continue;
+                    const float gt = row_sum(2 * pr, m), up = row_sum(2 * pr + 1, m);
+                    store(m, row >> 1, gt / (1.f + __expf(-gt)) * up);
+                }
+                return;
+            }
+            for (int i = lane; i < kRows * m_out; i += 32) {
+                const int rl = i & 15, m = i >> 4;
+                const int64_t row = row0 + rl;
+                if (row >= P.rows) continue;
+                store(m, row, row_sum(rl, m));
             }
         };
 
@@ -1081,6 +1096,7 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     L.m_x = m_x;
     L.x_split = x_split;
     L.y_f16 = y_dtype == APB_DTYPE_F16;
+    L.glu = (flags & APB_FLAG_GLU) ? 1 : 0;
     int items = 0, max_tiles = 0;
     int64_t cost = 0;
     const int esz = y_dtype == APB_DTYPE_F16 ? 2 : 4;

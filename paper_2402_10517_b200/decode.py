@@ -4,12 +4,14 @@ quantized linears (BASELINE config C5).
 Every linear of every decoder block (q/k/v/o, gate/up/down; arch.py:74-81 of
 the reference lists the same seven per block) is one n_max-bit bitplane parent
 served at a per-step bit-width k through the B200 GEMV (plan.GemvPlan, grouped
-q/k/v and gate/up launches, fp16 outputs, PDL chain).  The glue around them is
-three fused sm_100a kernels of csrc/apb_decode.cu (residual add + RMSNorm
-writing the next GEMV's activation buffer; RoPE + KV-cache append + split-chunk
-single-query attention writing the o-projection's activation buffer; SiLU*up),
-all in the GEMVs' PDL chain, plus a cuBLAS fp16 LM head; the whole step is
-captured in one CUDA graph per k.  Weights are random-init (codes uniform in [0, 2^n_max),
+q/k/v launch, fp16 outputs, PDL chain); gate and up are one layer with
+interleaved rows whose GEMV epilogue computes SiLU(gate)*up (APB_FLAG_GLU)
+straight into the down projection's input.  The glue around them is two fused
+sm_100a kernels of csrc/apb_decode.cu (residual add + RMSNorm writing the next
+GEMV's activation buffer; RoPE + KV-cache append + split-chunk single-query
+attention writing the o-projection's activation buffer), all in the GEMVs' PDL
+chain, plus a cuBLAS fp16 LM head; the whole step is captured in one CUDA graph
+per k.  Weights are random-init (codes uniform in [0, 2^n_max),
 sorted N(0,1) centroid rows, helpers.random_layer semantics), activations are
 real (embedding lookup of a token id, norms with unit weights).
 
@@ -66,8 +68,9 @@ class DecodeModel:
         g = torch.Generator(device="cuda").manual_seed(seed)
         self.blocks = []
         for _ in range(cfg.layers):
-            names = [("q", H, H), ("k", H, H), ("v", H, H), ("o", H, H), ("gate", I, H), ("up", I, H),
-                     ("down", H, I)]
+            # gate and up as ONE layer with interleaved rows (2i = gate_i, 2i+1 = up_i):
+            # the GEMV's GLU epilogue writes silu(gate) * up for the down projection
+            names = [("q", H, H), ("k", H, H), ("v", H, H), ("o", H, H), ("gate_up", 2 * I, H), ("down", H, I)]
             self.blocks.append({n: _random_prepared(torch, engine, r, c, cfg, g) for n, r, c in names})
         self.embed = (torch.randn(cfg.vocab, H, device="cuda", generator=g) * 0.02).half()
         self.lm_head = (torch.randn(cfg.vocab, H, device="cuda", generator=g) * 0.02).half()
@@ -100,9 +103,9 @@ class DecodeModel:
             qkv = plan.GemvPlan([blk["q"], blk["k"], blk["v"]], k, grouped=True, pdl=True, shared_x=True,
                                 y_fp16=True)
             o = plan.GemvPlan([blk["o"]], k, grouped=True, pdl=True, y_fp16=True)
-            gu = plan.GemvPlan([blk["gate"], blk["up"]], k, grouped=True, pdl=True, shared_x=True,
-                               y_fp16=True)
+            gu = plan.GemvPlan([blk["gate_up"]], k, grouped=True, pdl=True, y_fp16=True, glu=True)
             dn = plan.GemvPlan([blk["down"]], k, grouped=True, pdl=True, y_fp16=True)
+            gu.rebind(gu.x, dn.x)  # silu(gate) * up lands in the down projection's input
             per_block.append((qkv, o, gu, dn))
         self._plans[k] = per_block
         return per_block
@@ -129,8 +132,7 @@ class DecodeModel:
             o.run()
             check(lib.apb_rms_residual(P(self.resid), P(o.y[0]), P(self.norm_w), P(gu.x[0]), H, 1e-5, st),
                   "apb_rms_residual")
-            gu.run()
-            check(lib.apb_silu_mul(P(gu.y[0]), P(gu.y[1]), P(dn.x[0]), I, st), "apb_silu_mul")
+            gu.run()  # GLU epilogue: writes silu(gate) * up into dn.x
             dn.run()
             add = P(dn.y[0])
         check(lib.apb_rms_residual(P(self.resid), add, P(self.norm_w), P(self.hbuf), H, 1e-5, st),

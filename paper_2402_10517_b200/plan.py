@@ -16,6 +16,7 @@ from . import _device as dev
 from ._lib import (
     APB_DTYPE_F16,
     APB_DTYPE_F32,
+    APB_FLAG_GLU,
     APB_FLAG_PDL,
     check,
     int64_array,
@@ -32,7 +33,7 @@ def _ldx(cols: int) -> int:
 
 class GemvPlan:
     def __init__(self, preps, k: int, m: int = 1, grouped: bool = True, x_split: bool = False,
-                 y_fp16: bool = False, pdl: bool = False, shared_x: bool = False):
+                 y_fp16: bool = False, pdl: bool = False, shared_x: bool = False, glu: bool = False):
         torch = dev.require_cuda()
         for p in preps:
             if k not in p.tables16:
@@ -47,6 +48,12 @@ class GemvPlan:
         # programmatic dependent launch: safe here because the plan's weights
         # are never written by the kernels that precede it in a decode loop
         self.flags = APB_FLAG_PDL if pdl else 0
+        # glu: every layer's rows are interleaved (gate_i, up_i); y = silu(gate) * up
+        # with rows / 2 entries (the MLP's SiLU fused into the GEMV epilogue)
+        if glu:
+            if not grouped or any(p.tensor.rows % 2 for p in self.preps):
+                raise ParameterError("glu needs a grouped plan over layers with an even row count")
+            self.flags |= APB_FLAG_GLU
         ydt = torch.float16 if y_fp16 else torch.float32
         if shared_x:  # one activation for every layer (e.g. q/k/v, gate/up)
             cols = {p.tensor.cols for p in self.preps}
@@ -57,7 +64,8 @@ class GemvPlan:
         else:
             self.x = [torch.zeros((self.m_x, _ldx(p.tensor.cols)), dtype=torch.float16, device="cuda")
                       for p in self.preps]
-        self.y = [torch.zeros((m, p.tensor.rows), dtype=ydt, device="cuda") for p in self.preps]
+        out_rows = [p.tensor.rows // 2 if glu else p.tensor.rows for p in self.preps]
+        self.y = [torch.zeros((m, r), dtype=ydt, device="cuda") for r in out_rows]
         ts = [p.tensor for p in self.preps]
         n = len(ts)
         self._n = n
@@ -70,7 +78,7 @@ class GemvPlan:
         self._xp = ptr_array([dev.ptr(x) for x in self.x])
         self._ldx = int64_array([x.shape[1] for x in self.x])
         self._yp = ptr_array([dev.ptr(y) for y in self.y])
-        self._ldy = int64_array([t.rows for t in ts])
+        self._ldy = int64_array(out_rows)
         self._lib = load()
 
     def rebind(self, x_list, y_list):

@@ -22,6 +22,7 @@ def _reference_hidden(torch, engine, model, k):
     x = model.embed[model.token].view(H).float()
     for li, blk in enumerate(model.blocks):
         W = {n: engine.dequantize(p, k).float() for n, p in blk.items()}
+        W["gate"], W["up"] = W["gate_up"][0::2], W["gate_up"][1::2]  # interleaved rows
         h = rms(x).half().float()
         q, kk, v = (W[n] @ h for n in ("q", "k", "v"))
         q, kk = rope(q.half().float().view(nh, hd)), rope(kk.half().float().view(nh, hd))

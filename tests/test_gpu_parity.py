@@ -504,3 +504,33 @@ def test_tma_kernel_paths_vs_oracle(api, shape):
             want = ora.gemm(planes, cols, k, layer.centroid_tables[k], ora.prep_x(x, cols, fp16))
             err = ora.rel_err(y, want)
             assert err < TOL, (shape, k, m, fp16, err)
+
+
+@pytest.mark.parametrize("m,fp16", [(1, False), (1, True), (4, False)])
+def test_glu_epilogue_matches_silu_of_plain_outputs(api, m, fp16):
+    """APB_FLAG_GLU: interleaved (gate, up) rows -> silu(gate . x) * (up . x) from
+    the same fp32 row sums the plain launch produces (fp32: 1e-6; fp16 output:
+    one rounding of that value)."""
+    import torch
+
+    from paper_2402_10517_b200 import plan
+
+    _, _, engine, _ = api
+    prep = engine.prepare(_random_layer(api, 77, 2 * 1100, 2900))
+    for k in (3, 6):
+        glu = plan.GemvPlan([prep], k, m=m, grouped=True, y_fp16=fp16, glu=True)
+        ref = plan.GemvPlan([prep], k, m=m, grouped=True, y_fp16=False)
+        x = torch.randn(m, 2900, device="cuda", generator=torch.Generator(device="cuda").manual_seed(k)).half()
+        glu.x[0][:, :2900].copy_(x)
+        ref.x[0][:, :2900].copy_(x)
+        glu.run()
+        ref.run()
+        torch.cuda.synchronize()
+        y = ref.y[0]
+        want = torch.nn.functional.silu(y[:, 0::2]) * y[:, 1::2]
+        got = glu.y[0].float()
+        assert got.shape == (m, 1100)
+        if fp16:
+            assert torch.allclose(got, want.half().float(), rtol=2e-3, atol=1e-3), k
+        else:
+            assert torch.allclose(got, want, rtol=1e-5, atol=1e-5), k
