@@ -161,6 +161,33 @@ int apb_attention_decode(const uint16_t* q, const uint16_t* k, const uint16_t* v
                          int64_t workspace_bytes, uint16_t* out, const uint16_t* next_k_cache,
                          const uint16_t* next_v_cache, void* stream);
 
+/* ---- RMSNorm folded into the GEMV epilogues (decode step) ----
+ * rmsnorm(r) . w = s * (r . w) with the scalar s = rsqrt(mean(r^2) + eps), so
+ * W (rmsnorm(r) . w) = s * (W (r . w)):
+ *   mode 1 (producer, e.g. the o / down projection; m_x = 1, one problem, fp16
+ *     y): resid[i] += (W x)[i] (fp32), y[i] = fp16(resid[i] * norm_w[i]) -- the
+ *     next GEMV's activation -- and partials[cta] = this CTA's sum of resid^2
+ *     (partials: zero-filled once, n_partials >= the launch's grid -- 320
+ *     covers every grid on a 148-SM B200 -- else APB_ERR_PARAM);
+ *   mode 2 (consumer, e.g. q/k/v or gate/up): every row sum is multiplied by
+ *     s = rsqrt(sum(partials[0..min(n_partials, 320))) / norm_size + eps)
+ *     (summed in a fixed order: deterministic) before the GLU epilogue / the
+ *     store.
+ * TMA kernel only (k 3..8). */
+typedef struct {
+    int mode;               /* 0 none, 1 producer, 2 consumer */
+    float* resid;           /* mode 1: [rows] fp32 residual stream */
+    const uint16_t* norm_w; /* mode 1: [rows] fp16 RMSNorm weight */
+    float* partials;        /* mode 1: written; mode 2: read */
+    int n_partials;
+    int norm_size;          /* mode 2: hidden size */
+    float eps;              /* mode 2 */
+} apb_norm_epilogue;
+int apb_gemv_grouped_norm(int n_problems, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
+                          const int64_t* cols, const int64_t* padded_cols, int k, const uint16_t* const* lut,
+                          const uint16_t* const* x, int m_x, const int64_t* ldx, void* const* y, int y_dtype,
+                          const int64_t* ldy, const apb_norm_epilogue* norm, int flags, void* stream);
+
 /* ---- row-sharded GEMV with the all-gather fused in ----
  * apb_gemv_grouped_peers: apb_gemv_grouped over this rank's row slab (y[i] =
  * this rank's rows inside its full output) that also stores every y value at

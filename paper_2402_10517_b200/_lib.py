@@ -35,6 +35,14 @@ APB_DTYPE_F16 = 1
 APB_FLAG_PDL = 1
 APB_FLAG_GLU = 2
 
+
+class NormEpilogue(ctypes.Structure):
+    """apb_norm_epilogue (include/anyprec_b200.h)."""
+
+    _fields_ = [("mode", ctypes.c_int), ("resid", ctypes.c_void_p), ("norm_w", ctypes.c_void_p),
+                ("partials", ctypes.c_void_p), ("n_partials", ctypes.c_int), ("norm_size", ctypes.c_int),
+                ("eps", ctypes.c_float)]
+
 # Every symbol declared in include/anyprec_b200.h, with its ctypes signature.
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -60,6 +68,10 @@ SIGNATURES = {
     "apb_rms_residual": ([_P, _P, _P, _P, _I64, ctypes.c_float, _P], _I),
     "apb_rope_cache": ([_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I64, _P], _I),
     "apb_silu_mul": ([_P, _P, _P, _I64, _P], _I),
+    "apb_gemv_grouped_norm": (
+        [_I, _PP, _PI, _PI64, _PI64, _PI64, _I, _PP, _PP, _I, _PI64, _PP, _I, _PI64, _P, _I, _P],
+        _I,
+    ),
     "apb_gemv_grouped_peers": (
         [_I, _PP, _PI, _PI64, _PI64, _PI64, _I, _PP, _PP, _I, _PI64, _I, _PP, _I, _PI64, _I, _PP, _PP, _I, _P],
         _I,

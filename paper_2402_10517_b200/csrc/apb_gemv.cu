@@ -1108,7 +1108,8 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
                              const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
                              const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split,
                              void* const* y, int y_dtype, const int64_t* ldy, int64_t y_off, int flags, void* stream, int n_peers,
-                             void* const* y_peers, uint32_t* const* peer_flags);
+                             void* const* y_peers, uint32_t* const* peer_flags,
+                             const apb_norm_epilogue* norm);
 
 extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, const int* n_max,
                                 const int64_t* rows, const int64_t* cols,
@@ -1134,7 +1135,7 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
     cudaStream_t s = (cudaStream_t)stream;
     if (m_x <= 8 && n_problems <= 16) {  // TMA-fed kernel (apb_gemv7.cu)
         const int rc = apb7_try_gemv(n_problems, planes, n_max, rows, cols, padded_cols, k, lut, x, m_x, ldx, 0,
-                                     x_split, y, y_dtype, ldy, 0, flags, stream, 0, nullptr, nullptr);
+                                     x_split, y, y_dtype, ldy, 0, flags, stream, 0, nullptr, nullptr, nullptr);
         if (rc != -1) return rc;
     }
     if (glu) return APB_ERR_PARAM;  // the gate/up epilogue exists on the TMA kernel only
@@ -1186,8 +1187,42 @@ extern "C" int apb_gemv_grouped_peers(int n_problems, const uint8_t* const* plan
             if (!y_peers[(size_t)i * n_peers + j]) return APB_ERR_PARAM;
     }
     const int rc = apb7_try_gemv(n_problems, planes, n_max, rows, cols, padded_cols, k, lut, x, m_x, ldx, 0,
-                                 x_split, y, y_dtype, ldy, 0, flags, stream, n_peers, y_peers, peer_flags);
+                                 x_split, y, y_dtype, ldy, 0, flags, stream, n_peers, y_peers, peer_flags,
+                                 nullptr);
     return rc == -1 ? APB_ERR_PARAM : rc;  // e.g. more than 64K columns: not on the fused path
+}
+
+// Decode-step RMSNorm folded into the GEMV epilogues (see apb_norm_epilogue).
+extern "C" int apb_gemv_grouped_norm(int n_problems, const uint8_t* const* planes, const int* n_max,
+                                     const int64_t* rows, const int64_t* cols, const int64_t* padded_cols, int k,
+                                     const uint16_t* const* lut, const uint16_t* const* x, int m_x,
+                                     const int64_t* ldx, void* const* y, int y_dtype, const int64_t* ldy,
+                                     const apb_norm_epilogue* norm, int flags, void* stream) {
+    if (!norm || norm->mode < 0 || norm->mode > 2) return APB_ERR_PARAM;
+    if (n_problems < 1 || n_problems > 16) return APB_ERR_SHAPE;
+    if (k < 3 || k > 8 || (y_dtype != APB_DTYPE_F16 && y_dtype != APB_DTYPE_F32)) return APB_ERR_PARAM;
+    if (m_x < 1 || m_x > 8) return APB_ERR_SHAPE;
+    const bool glu = (flags & APB_FLAG_GLU) != 0;
+    if (norm->mode == 1) {  // producer: one batch row, one problem, fp16 normalised output
+        if (m_x != 1 || n_problems != 1 || glu || y_dtype != APB_DTYPE_F16) return APB_ERR_PARAM;
+        if (!norm->resid || !norm->norm_w || !norm->partials) return APB_ERR_PARAM;
+        if (norm->n_partials < 1) return APB_ERR_PARAM;  // checked against the launch grid later
+    }
+    if (norm->mode == 2 && (!norm->partials || norm->n_partials <= 0 || norm->norm_size <= 0))
+        return APB_ERR_PARAM;
+    for (int i = 0; i < n_problems; ++i) {
+        if (rows[i] <= 0 || cols[i] <= 0 || (glu && (rows[i] & 1))) return APB_ERR_SHAPE;
+        if (padded_cols[i] != apb_pad_columns(cols[i])) return APB_ERR_SHAPE;
+        if (k > n_max[i] || n_max[i] > 8) return APB_ERR_PARAM;
+        if (ldx[i] < cols[i] || (ldx[i] % 8) != 0) return APB_ERR_PARAM;
+        if (!planes[i] || !lut[i] || !x[i] || !y[i]) return APB_ERR_PARAM;
+        if (((uintptr_t)x[i] & 15) != 0 || ((uintptr_t)planes[i] & 15) != 0) return APB_ERR_PARAM;
+        if (((uintptr_t)lut[i] & 15) != 0) return APB_ERR_PARAM;
+        if (ldy[i] < (glu ? rows[i] / 2 : rows[i])) return APB_ERR_SHAPE;
+    }
+    const int rc = apb7_try_gemv(n_problems, planes, n_max, rows, cols, padded_cols, k, lut, x, m_x, ldx, 0, 0, y,
+                                 y_dtype, ldy, 0, flags, stream, 0, nullptr, nullptr, norm);
+    return rc == -1 ? APB_ERR_PARAM : rc;
 }
 
 #ifdef APB_TIMELINE

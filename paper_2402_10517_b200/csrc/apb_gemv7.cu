@@ -48,6 +48,7 @@ using apb::prmt;
 constexpr int kRows = 16;      // rows per item
 constexpr int kMaxProb = 16;   // problems per grouped launch
 constexpr int kMaxPeers = 8;   // fused all-gather: ranks of one NVSwitch node
+constexpr int kMaxPartials = 320;  // RMSNorm epilogue: >= the largest grid (2 CTAs x 148 SMs)
 constexpr int kSmemBase = 1024;  // sm_100 reserves the first 1 KB of the shared window
 constexpr int kMaxCols = 64 * 1024;  // padded columns per layer on this path
 
@@ -91,6 +92,14 @@ struct alignas(64) Launch7 {
     int64_t total_cost;
     int m_x, x_split, y_f16;
     int glu;           // APB_FLAG_GLU: interleaved (gate, up) rows -> silu(gate) * up
+    // RMSNorm folded into the epilogues (apb_gemv_grouped_norm): 1 = producer
+    // (resid += y; y_out = fp16(resid * norm_w); partials[cta] = sum resid^2),
+    // 2 = consumer (row sums scaled by rsqrt(sum(partials) / norm_size + eps))
+    int norm_mode, n_partials, norm_size;
+    float norm_eps;
+    float* resid;
+    const __half* norm_w;
+    float* partials;
     int n_stages;      // ring depth
     int64_t xs_bytes;  // one activation buffer
     int x_bufs;        // 1 when every problem shares one x, else 2
@@ -313,12 +322,16 @@ __device__ __forceinline__ void decode_word(const uint32_t* Q, uint32_t off, uin
 // NB = batch pairs per launch (m_x <= 2 NB).  NB = 1 stages x in shared memory;
 // NB > 1 (small-batch GEMM, engine.py:312-341 with M <= 8) reads its B
 // fragments from global memory (L1 / L2 resident) so x never limits smem.
-template <int K, int NB, int CPS>
+// EPI: the epilogue features (GLU, RMSNorm fold, fused all-gather) are compiled
+// in; plain launches use the EPI = false instantiation, whose reduce is exactly
+// the plain one (measured: the unused branches cost small launches ~2-3 %).
+template <int K, int NB, int CPS, bool EPI>
 __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(const __grid_constant__ Launch7 L) {
     using G = Geo<K, NB, CPS>;
     constexpr int WC = G::kWC, NG = G::kNG;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ep_glu = EPI ? L.glu : 0, ep_norm = EPI ? L.norm_mode : 0, ep_peers = EPI ? L.n_peers : -1;
     if (saddr(smem) != kSmemBase) __trap();  // lds_table folds the table base into the immediate
 
     const int first = item_at_cost(L, L.total_cost * (int64_t)blockIdx.x / gridDim.x);
@@ -538,6 +551,9 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
         // ========================= service: tables, x, y =========================
         const int g = lane >> 2, q = lane & 3, rho = 2 * g + (q >> 1);
         uint32_t y_written = 0;  // y values this lane stored (fused all-gather accounting)
+        float norm_scale = 1.f;  // norm_mode 2: the producer's RMSNorm factor
+        float sq_acc = 0.f;      // norm_mode 1: this lane's sum of resid^2
+        float resid_pre = 0.f;   // norm_mode 1: resid of row (item row0 + lane), prefetched
         auto reduce = [&](int item, int pi, int slot) {
             const Prob7& P = L.prob[pi];
             const int m_out = L.x_split ? (L.m_x >> 1) : L.m_x;
@@ -562,19 +578,19 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                 if (L.y_f16) {
                     const __half hv = __float2half_rn(v);
                     reinterpret_cast<__half*>(P.y)[off] = hv;
-                    for (int j = 0; j < L.n_peers; ++j) reinterpret_cast<__half*>(L.y_peer[pi][j])[off] = hv;
+                    for (int j = 0; j < ep_peers; ++j) reinterpret_cast<__half*>(L.y_peer[pi][j])[off] = hv;
                 } else {
                     reinterpret_cast<float*>(P.y)[off] = v;
-                    for (int j = 0; j < L.n_peers; ++j) reinterpret_cast<float*>(L.y_peer[pi][j])[off] = v;
+                    for (int j = 0; j < ep_peers; ++j) reinterpret_cast<float*>(L.y_peer[pi][j])[off] = v;
                 }
                 ++y_written;
             };
-            if (L.glu) {  // rows (2i, 2i+1) = (gate_i, up_i): y[i] = silu(gate_i . x) * (up_i . x)
+            if (ep_glu) {  // rows (2i, 2i+1) = (gate_i, up_i): y[i] = silu(gate_i . x) * (up_i . x)
                 for (int i = lane; i < (kRows / 2) * m_out; i += 32) {
                     const int pr = i & 7, m = i >> 3;
                     const int64_t row = row0 + 2 * pr;
                     if (row >= P.rows) continue;
-                    const float gt = row_sum(2 * pr, m), up = row_sum(2 * pr + 1, m);
+                    const float gt = norm_scale * row_sum(2 * pr, m), up = norm_scale * row_sum(2 * pr + 1, m);
                     store(m, row >> 1, gt / (1.f + __expf(-gt)) * up);
                 }
                 return;
@@ -583,7 +599,14 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                 const int rl = i & 15, m = i >> 4;
                 const int64_t row = row0 + rl;
                 if (row >= P.rows) continue;
-                store(m, row, row_sum(rl, m));
+                if (ep_norm == 1) {  // residual add + the next RMSNorm's numerator (m_out == 1)
+                    const float rs = resid_pre + row_sum(rl, m);  // lane == rl: loaded during the compute
+                    __stcg(L.resid + row, rs);
+                    sq_acc += rs * rs;
+                    store(m, row, rs * __half2float(L.norm_w[row]));
+                } else {
+                    store(m, row, norm_scale * row_sum(rl, m));
+                }
             }
         };
 
@@ -606,10 +629,31 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
 #pragma unroll 1
         for (int jl = 0; jl < n_local + 2; ++jl) {
             if (jl >= 2) {  // item jl-2 done by every compute warp: reduce it, free its slot
+                if (ep_norm == 1) {  // residual rows of this item, fetched while it is computed
+                    if (!waited) {
+                        asm volatile("griddepcontrol.wait;" ::: "memory");
+                        waited = true;
+                    }
+                    const Prob7& P = L.prob[pi_hist[jl & 1]];
+                    const int64_t row = (int64_t)(first + jl - 2 - P.item_begin) * kRows + lane;
+                    resid_pre = lane < kRows && row < P.rows ? __ldcg(L.resid + row) : 0.f;
+                }
                 mbar_wait(b_idone + 8 * (jl & 1), ((jl - 2) >> 1) & 1);
                 if (!waited) {  // y of earlier kernels (PDL); compute warp 0 already waited
                     asm volatile("griddepcontrol.wait;" ::: "memory");
                     waited = true;
+                    if (ep_norm == 2) {  // the producer's per-CTA sums of resid^2, fixed order
+                        float pv[kMaxPartials / 32];  // one batch of loads in flight
+#pragma unroll
+                        for (int u = 0; u < kMaxPartials / 32; ++u)
+                            pv[u] = lane + 32 * u < L.n_partials ? __ldcg(L.partials + lane + 32 * u) : 0.f;
+                        float acc = 0.f;
+#pragma unroll
+                        for (int u = 0; u < kMaxPartials / 32; ++u) acc += pv[u];
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                        norm_scale = rsqrtf(acc / (float)L.norm_size + L.norm_eps);
+                    }
                 }
                 reduce(first + jl - 2, pi_hist[jl & 1], jl & 1);
             }
@@ -644,7 +688,12 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                 if (jl == 0 && lane == 0) APB_TL(1);
             }
         }
-        if (L.n_peers >= 0) {
+        if (ep_norm == 1) {  // this CTA's share of the next RMSNorm's sum of squares
+#pragma unroll
+            for (int o = 16; o; o >>= 1) sq_acc += __shfl_xor_sync(0xffffffffu, sq_acc, o);
+            if (lane == 0) __stcg(L.partials + blockIdx.x, sq_acc);
+        }
+        if (ep_peers >= 0) {
             // publish: every lane's local + peer stores visible system-wide, then
             // one release-add per rank of the values this CTA wrote
             __threadfence_system();
@@ -652,7 +701,7 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
 #pragma unroll
             for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
             __syncwarp();
-            if (lane <= L.n_peers && tot > 0)  // peers' counters, then this rank's own
+            if (lane <= ep_peers && tot > 0)  // peers' counters, then this rank's own
                 asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(L.peer_flag[lane]), "r"(tot) : "memory");
         }
         if (lane == 0) APB_TL(5);
@@ -1031,7 +1080,7 @@ static int choose_cps(const Launch7& L) {
     return fits2 && (K == 3 || !long_launch) ? 2 : 1;
 }
 
-template <int K, int NB, int CPS>
+template <int K, int NB, int CPS, bool EPI>
 static int launch(Launch7& L, int flags, cudaStream_t s) {
     using G = Geo<K, NB, CPS>;
     const size_t limit = CPS == 2 ? kSmemLimit2 : kSmemLimit;
@@ -1040,7 +1089,7 @@ static int launch(Launch7& L, int flags, cudaStream_t s) {
     while (nst >= G::kNG && G::total(nst, L.x_bufs * L.xs_bytes) > limit) --nst;
     if (nst < G::kNG || nst < 3) return -1;
     L.n_stages = nst;
-    auto kern = gemv7_kernel<K, NB, CPS>;
+    auto kern = gemv7_kernel<K, NB, CPS, EPI>;
     static std::atomic<int> configured{0};
     if (!configured.load(std::memory_order_acquire)) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit) != cudaSuccess)
@@ -1049,6 +1098,7 @@ static int launch(Launch7& L, int flags, cudaStream_t s) {
     }
     int grid = CPS * sm_count();
     if (grid > L.n_items) grid = L.n_items;
+    if (L.norm_mode == 1 && grid > L.n_partials) return APB_ERR_PARAM;  // a CTA without a partials slot
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3((unsigned)G::kThreads);
@@ -1079,7 +1129,8 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
                              const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
                              const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split,
                              void* const* y, int y_dtype, const int64_t* ldy, int64_t y_off, int flags, void* stream,
-                             int n_peers, void* const* y_peers, uint32_t* const* peer_flags) {
+                             int n_peers, void* const* y_peers, uint32_t* const* peer_flags,
+                             const apb_norm_epilogue* norm) {
     using namespace apb7;
     static const bool disabled = [] {
         const char* e = std::getenv("APB_GEMV_V7");
@@ -1097,6 +1148,15 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     L.x_split = x_split;
     L.y_f16 = y_dtype == APB_DTYPE_F16;
     L.glu = (flags & APB_FLAG_GLU) ? 1 : 0;
+    if (norm && norm->mode) {
+        L.norm_mode = norm->mode;
+        L.resid = norm->resid;
+        L.norm_w = reinterpret_cast<const __half*>(norm->norm_w);
+        L.partials = norm->partials;
+        L.n_partials = norm->n_partials < kMaxPartials ? norm->n_partials : kMaxPartials;
+        L.norm_size = norm->norm_size;
+        L.norm_eps = norm->eps;
+    }
     int items = 0, max_tiles = 0;
     int64_t cost = 0;
     const int esz = y_dtype == APB_DTYPE_F16 ? 2 : 4;
@@ -1148,12 +1208,13 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
 #endif
     const int nb = m_x <= 2 ? 1 : (m_x <= APB7_NB2_MAX ? 2 : 4);
     if (nb > 1) L.xs_bytes = 0;
+    const bool epi = L.glu || L.norm_mode || L.n_peers >= 0;
     switch (k * 8 + nb) {
-#define APB7_CASE(K)                                                                                  \
-    case K * 8 + 1:                                                                                   \
-        return choose_cps<K, 1>(L) == 2 ? launch<K, 1, 2>(L, flags, s) : launch<K, 1, 1>(L, flags, s); \
-    case K * 8 + 2: return launch<K, 2, 1>(L, flags, s);                                               \
-    case K * 8 + 4: return launch<K, 4, 1>(L, flags, s);
+#define APB7_L(K, NB, CPS) (epi ? launch<K, NB, CPS, true>(L, flags, s) : launch<K, NB, CPS, false>(L, flags, s))
+#define APB7_CASE(K)                                                           \
+    case K * 8 + 1: return choose_cps<K, 1>(L) == 2 ? APB7_L(K, 1, 2) : APB7_L(K, 1, 1); \
+    case K * 8 + 2: return APB7_L(K, 2, 1);                                    \
+    case K * 8 + 4: return APB7_L(K, 4, 1);
         APB7_CASE(3)
         APB7_CASE(4)
         APB7_CASE(5)
@@ -1161,6 +1222,7 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
         APB7_CASE(7)
         APB7_CASE(8)
 #undef APB7_CASE
+#undef APB7_L
     }
     return -1;
 }

@@ -87,6 +87,10 @@ class DecodeModel:
         ws_bytes = load().apb_attention_decode_workspace(nh, hd, context + 1)
         self.attn_ws = torch.zeros(ws_bytes, device="cuda", dtype=torch.uint8)
         self.hbuf = torch.zeros(1, H, device="cuda", dtype=torch.float16)
+        # per-CTA sums of squares of the two RMSNorm producers of a block (zero-filled
+        # once; a CTA index is written by the same launch shape every step)
+        self.part_a = torch.zeros(320, device="cuda", dtype=torch.float32)
+        self.part_b = torch.zeros(320, device="cuda", dtype=torch.float32)
         self.token = torch.zeros(1, dtype=torch.long, device="cuda")
         self.next_token = torch.zeros(1, dtype=torch.long, device="cuda")
         self.kv_prefetch = True
@@ -95,18 +99,30 @@ class DecodeModel:
 
     # ---- per-k launch plans: x / y buffers shared by every block -----------------
     def _plans_for(self, k: int):
+        """Per block: qkv | o | gate_up | down.  RMSNorm lives in the epilogues:
+        o and down are producers (residual add, fp16(resid * w) straight into the
+        next GEMV's activation buffer, per-CTA sums of squares), q/k/v (from block
+        1 on) and gate_up are consumers (row sums scaled by the norm factor)."""
         if k in self._plans:
             return self._plans[k]
-        plan = self._plan_mod
+        plan, cfg = self._plan_mod, self.cfg
+        H, eps = cfg.hidden, 1e-5
         per_block = []
-        for blk in self.blocks:
+        for li, blk in enumerate(self.blocks):
+            qkv_norm = None if li == 0 else ("consumer", self.part_b, H, eps)
             qkv = plan.GemvPlan([blk["q"], blk["k"], blk["v"]], k, grouped=True, pdl=True, shared_x=True,
-                                y_fp16=True)
-            o = plan.GemvPlan([blk["o"]], k, grouped=True, pdl=True, y_fp16=True)
-            gu = plan.GemvPlan([blk["gate_up"]], k, grouped=True, pdl=True, y_fp16=True, glu=True)
-            dn = plan.GemvPlan([blk["down"]], k, grouped=True, pdl=True, y_fp16=True)
+                                y_fp16=True, norm=qkv_norm)
+            o = plan.GemvPlan([blk["o"]], k, grouped=True, pdl=True, y_fp16=True,
+                              norm=("producer", self.resid, self.norm_w, self.part_a))
+            gu = plan.GemvPlan([blk["gate_up"]], k, grouped=True, pdl=True, y_fp16=True, glu=True,
+                               norm=("consumer", self.part_a, H, eps))
+            dn = plan.GemvPlan([blk["down"]], k, grouped=True, pdl=True, y_fp16=True,
+                               norm=("producer", self.resid, self.norm_w, self.part_b))
+            o.rebind(o.x, gu.x)    # fp16(resid * w) after the attention block -> gate_up's input
             gu.rebind(gu.x, dn.x)  # silu(gate) * up lands in the down projection's input
             per_block.append((qkv, o, gu, dn))
+        for (_, _, _, dn), (qkv, _, _, _) in zip(per_block, per_block[1:]):
+            dn.rebind(dn.x, qkv.x[:1])  # fp16(resid * w) after the MLP -> the next block's q/k/v input
         self._plans[k] = per_block
         return per_block
 
@@ -116,26 +132,23 @@ class DecodeModel:
 
         lib, st = load(), dev.stream_ptr()
         cfg, ctx = self.cfg, self.context
-        nh, hd, H, I = cfg.heads, cfg.head_dim, cfg.hidden, cfg.intermediate
+        nh, hd, H = cfg.heads, cfg.head_dim, cfg.hidden
         P = dev.ptr
         self.resid.copy_(self.embed[self.token].view(H).float())
-        add = None
-        for li, (qkv, o, gu, dn) in enumerate(self._plans_for(k)):
-            check(lib.apb_rms_residual(P(self.resid), add, P(self.norm_w), P(qkv.x[0]), H, 1e-5, st),
-                  "apb_rms_residual")
+        blocks = self._plans_for(k)
+        check(lib.apb_rms_residual(P(self.resid), None, P(self.norm_w), P(blocks[0][0].x[0]), H, 1e-5, st),
+              "apb_rms_residual")
+        for li, (qkv, o, gu, dn) in enumerate(blocks):
             qkv.run()
             check(lib.apb_attention_decode(P(qkv.y[0]), P(qkv.y[1]), P(qkv.y[2]), P(self.cos), P(self.sin),
                                            P(self.k_cache[li]), P(self.v_cache[li]), nh, hd, (ctx + 1) * hd, ctx,
                                            hd ** -0.5, P(self.attn_ws), self.attn_ws.numel(), P(o.x[0]),
                                            *self._next_kv(li), st),
                   "apb_attention_decode")
-            o.run()
-            check(lib.apb_rms_residual(P(self.resid), P(o.y[0]), P(self.norm_w), P(gu.x[0]), H, 1e-5, st),
-                  "apb_rms_residual")
-            gu.run()  # GLU epilogue: writes silu(gate) * up into dn.x
-            dn.run()
-            add = P(dn.y[0])
-        check(lib.apb_rms_residual(P(self.resid), add, P(self.norm_w), P(self.hbuf), H, 1e-5, st),
+            o.run()   # resid += o(att); gate_up's input = fp16(resid * w)
+            gu.run()  # scaled by the norm factor; GLU epilogue -> dn.x
+            dn.run()  # resid += down(.); the next block's input = fp16(resid * w)
+        check(lib.apb_rms_residual(P(self.resid), None, P(self.norm_w), P(self.hbuf), H, 1e-5, st),
               "apb_rms_residual")
         logits = self.hbuf @ self.lm_head.t()
         self.next_token.copy_(torch.argmax(logits, dim=-1))

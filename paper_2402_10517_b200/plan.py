@@ -33,7 +33,8 @@ def _ldx(cols: int) -> int:
 
 class GemvPlan:
     def __init__(self, preps, k: int, m: int = 1, grouped: bool = True, x_split: bool = False,
-                 y_fp16: bool = False, pdl: bool = False, shared_x: bool = False, glu: bool = False):
+                 y_fp16: bool = False, pdl: bool = False, shared_x: bool = False, glu: bool = False,
+                 norm=None):
         torch = dev.require_cuda()
         for p in preps:
             if k not in p.tables16:
@@ -64,6 +65,22 @@ class GemvPlan:
         else:
             self.x = [torch.zeros((self.m_x, _ldx(p.tensor.cols)), dtype=torch.float16, device="cuda")
                       for p in self.preps]
+        # norm: None, or ("producer", resid f32, norm_w f16, partials f32) / ("consumer",
+        # partials f32, norm_size, eps) -- RMSNorm folded into the epilogue
+        # (apb_gemv_grouped_norm)
+        self._norm = None
+        if norm is not None:
+            from ._lib import NormEpilogue
+
+            if norm[0] == "producer":
+                _, resid, w, part = norm
+                self._norm = NormEpilogue(1, dev.ptr(resid), dev.ptr(w), dev.ptr(part), part.numel(), 0, 0.0)
+            elif norm[0] == "consumer":
+                _, part, size, eps = norm
+                self._norm = NormEpilogue(2, None, None, dev.ptr(part), part.numel(), int(size), float(eps))
+            else:
+                raise ParameterError(f"unknown norm epilogue {norm[0]!r}")
+            self._norm_keep = norm  # the buffers must outlive the plan
         out_rows = [p.tensor.rows // 2 if glu else p.tensor.rows for p in self.preps]
         self.y = [torch.zeros((m, r), dtype=ydt, device="cuda") for r in out_rows]
         ts = [p.tensor for p in self.preps]
@@ -106,6 +123,13 @@ class GemvPlan:
     def run(self):
         s = dev.stream_ptr()
         L = self._lib
+        if self._norm is not None:
+            P = lambda a: ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))  # noqa: E731
+            check(L.apb_gemv_grouped_norm(self._n, P(self._planes), self._nmax, self._rows, self._cols,
+                                          self._padded, self.k, P(self._lut), P(self._xp), self.m_x, self._ldx,
+                                          P(self._yp), self.y_dtype, self._ldy, ctypes.byref(self._norm),
+                                          self.flags, s), "apb_gemv_grouped_norm")
+            return
         if self.grouped:
             check(
                 L.apb_gemv_grouped(self._n, ctypes.cast(self._planes, ctypes.POINTER(ctypes.c_void_p)),
