@@ -534,3 +534,49 @@ def test_glu_epilogue_matches_silu_of_plain_outputs(api, m, fp16):
             assert torch.allclose(got, want.half().float(), rtol=2e-3, atol=1e-3), k
         else:
             assert torch.allclose(got, want, rtol=1e-5, atol=1e-5), k
+
+
+def test_norm_epilogues_producer_and_consumer(api):
+    """apb_gemv_grouped_norm: the producer adds W.x to the fp32 residual,
+    writes fp16(resid * w) and per-CTA sums of squares (their total = sum
+    resid^2); the consumer scales every row sum by rsqrt(total / n + eps) -- also
+    before the GLU epilogue."""
+    import torch
+
+    from paper_2402_10517_b200 import plan
+
+    _, _, engine, _ = api
+    H = 2048
+    prod = engine.prepare(_random_layer(api, 91, H, 1500))
+    cons = engine.prepare(_random_layer(api, 92, 2 * 700, H))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    resid0 = torch.randn(H, device="cuda", generator=g)
+    w = (torch.rand(H, device="cuda", generator=g) + 0.5).half()
+    part = torch.zeros(320, device="cuda")
+    for k in (3, 7):
+        resid = resid0.clone()
+        p = plan.GemvPlan([prod], k, grouped=True, y_fp16=True, norm=("producer", resid, w, part))
+        ref = plan.GemvPlan([prod], k, grouped=True, y_fp16=False)
+        x = torch.randn(1, 1500, device="cuda", generator=g).half()
+        p.x[0][:, :1500].copy_(x)
+        ref.x[0][:, :1500].copy_(x)
+        p.run()
+        ref.run()
+        torch.cuda.synchronize()
+        want_r = resid0 + ref.y[0][0]
+        assert torch.allclose(resid, want_r, rtol=0, atol=1e-5)
+        assert torch.equal(p.y[0][0], (resid * w.float()).half())
+        assert abs(float(part.sum()) - float((resid * resid).sum())) <= 1e-4 * float((resid * resid).sum())
+        s = float(torch.rsqrt((resid * resid).sum() / H + 1e-5))
+        # consumer (plain and GLU) fed the producer's output
+        c = plan.GemvPlan([cons], k, grouped=True, y_fp16=False, norm=("consumer", part, H, 1e-5))
+        cg = plan.GemvPlan([cons], k, grouped=True, y_fp16=False, glu=True, norm=("consumer", part, H, 1e-5))
+        cr = plan.GemvPlan([cons], k, grouped=True, y_fp16=False)
+        for q in (c, cg, cr):
+            q.x[0][:, :H].copy_(p.y[0])
+            q.run()
+        torch.cuda.synchronize()
+        plain = cr.y[0][0]
+        assert torch.allclose(c.y[0][0], s * plain, rtol=1e-5, atol=1e-5)
+        gl = torch.nn.functional.silu(s * plain[0::2]) * (s * plain[1::2])
+        assert torch.allclose(cg.y[0][0], gl, rtol=1e-5, atol=1e-5)
