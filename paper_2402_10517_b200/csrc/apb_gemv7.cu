@@ -347,6 +347,22 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
     uint8_t* const xs = smem + G::kRing + (size_t)NST * G::kStageBytes;  // [2][m_x][padded] fp16
     float* const red = reinterpret_cast<float*>(xs + L.x_bufs * L.xs_bytes);
     const uint32_t bar = saddr(reinterpret_cast<uint8_t*>(red) + G::kRedBytes);
+    // spare word after the barriers: the consumer RMSNorm factor (norm_mode 2),
+    // computed by compute warp 0 while x is in flight, read by the service warp
+    float* const s_norm = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(red) + G::kRedBytes + 16 * NST + 80);
+    // the producer's per-CTA sums of resid^2 -> rsqrt(mean + eps), fixed order (one warp)
+    auto norm_factor = [&]() {
+        float pv[kMaxPartials / 32];
+#pragma unroll
+        for (int u = 0; u < kMaxPartials / 32; ++u)
+            pv[u] = lane + 32 * u < L.n_partials ? __ldcg(L.partials + lane + 32 * u) : 0.f;
+        float acc = 0.f;
+#pragma unroll
+        for (int u = 0; u < kMaxPartials / 32; ++u) acc += pv[u];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) *s_norm = rsqrtf(acc / (float)L.norm_size + L.norm_eps);
+    };
     // barriers (8 B each): full[NST] | empty[NST] | lut_full[2] | lut_empty[2] | table_ready[2] | item_done[2] | x_full[2]
     const uint32_t b_full = bar, b_empty = bar + 8 * NST, b_lfull = bar + 16 * NST, b_lempty = b_lfull + 16,
                    b_tready = b_lfull + 32, b_idone = b_lfull + 48, b_xfull = b_lfull + 64;
@@ -642,18 +658,7 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                 if (!waited) {  // y of earlier kernels (PDL); compute warp 0 already waited
                     asm volatile("griddepcontrol.wait;" ::: "memory");
                     waited = true;
-                    if (ep_norm == 2) {  // the producer's per-CTA sums of resid^2, fixed order
-                        float pv[kMaxPartials / 32];  // one batch of loads in flight
-#pragma unroll
-                        for (int u = 0; u < kMaxPartials / 32; ++u)
-                            pv[u] = lane + 32 * u < L.n_partials ? __ldcg(L.partials + lane + 32 * u) : 0.f;
-                        float acc = 0.f;
-#pragma unroll
-                        for (int u = 0; u < kMaxPartials / 32; ++u) acc += pv[u];
-#pragma unroll
-                        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                        norm_scale = rsqrtf(acc / (float)L.norm_size + L.norm_eps);
-                    }
+                    if (ep_norm == 2) norm_scale = *s_norm;  // written by compute warp 0 before item 0 was done
                 }
                 reduce(first + jl - 2, pi_hist[jl & 1], jl & 1);
             }
@@ -739,7 +744,10 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
 #pragma unroll
             for (int c2 = 0; c2 < 2; ++c2) acc[c2][0] = acc[c2][1] = acc[c2][2] = acc[c2][3] = 0.f;
             mbar_sleep(b_tready + 8 * (jl & 1), (jl >> 1) & 1);
-            if (jl == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // x from the previous kernel
+            if (jl == 0) {
+                asm volatile("griddepcontrol.wait;" ::: "memory");  // x from the previous kernel
+                if (ep_norm == 2 && warp == 0) norm_factor();
+            }
 #pragma unroll 1
             for (; gs < item_gs + nt; gs += NG) {
                 const int tile = gs - item_gs;
@@ -899,11 +907,13 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                         issue_x_one(pi, 0);
                         APB_TL(2);
                     }
+                    if (ep_norm == 2) norm_factor();  // overlaps the x copy
                 }
                 mbar_sleep(b_xfull + 8 * xb, (xph >> xb) & 1u);
                 xph ^= 1u << xb;
             } else if (jl == 0) {
                 asm volatile("griddepcontrol.wait;" ::: "memory");  // x from the previous kernel
+                if (ep_norm == 2 && warp == 0) norm_factor();
             }
         }
 #pragma unroll 1

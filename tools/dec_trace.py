@@ -29,11 +29,12 @@ print(f"k={k} kernels/step={len(ev)} span={span:.0f}us")
 for nme in sorted(tot, key=lambda x: -tot[x]):
     print(f"{nme:60s} n={cnt[nme]:4d} dur={tot[nme]:8.1f}us gap_before={gap[nme]:8.1f}us")
 
-print("--- one block (middle of the step): start offset / duration us")
+print('--- one block (middle of the step): start offset / duration us')
 i0 = len(ev) // 2
-while 'rms_residual' not in ev[i0]['name']:
+while 'attention' not in ev[i0]['name']:
     i0 += 1
+i0 -= 1  # the q/k/v GEMV before it
 t0 = ev[i0]['ts']
-for e in ev[i0:i0 + 9]:
+for e in ev[i0:i0 + 6]:
     nm = e['name'].replace('(anonymous namespace)::', '').split('(')[0][:40]
     print(f"{nm:40s} start={e['ts'] - t0:8.2f} dur={e['dur']:7.2f} end={e['ts'] + e['dur'] - t0:8.2f}")
