@@ -263,19 +263,24 @@ def run_ours(args):
                 for j, li in enumerate(grp):
                     gather_rows(p.y[j], SHAPES[li][1])
 
-    # warm-up (also configures kernel attributes before capture)
-    for _ in range(max(3, args.warmup)):
+    if fused is not None:  # self-check: one aligned step, short waits, every rank saw every arrival
+        for sp in fused:
+            sp._spin = 1 << 18  # ~40 ms per wait at most
+        dist.barrier()
         step()
-    torch.cuda.synchronize()
-    if fused is not None:  # self-check: every rank saw every arrival in time
+        torch.cuda.synchronize()
         bad = torch.tensor([max(sp.gather.status() for sp in fused)], device="cuda", dtype=torch.int32)
         dist.all_reduce(bad, op=dist.ReduceOp.MAX)
         if int(bad.item()):
             print("[bench] fused gather self-check failed; using NCCL", file=sys.stderr)
             fused, gather_mode = None, "nccl all_gather_into_tensor after each GEMV (fused self-check failed)"
-            for _ in range(max(3, args.warmup)):
-                step()
-            torch.cuda.synchronize()
+        else:
+            for sp in fused:
+                sp._spin = 1 << 26
+    # warm-up (also configures kernel attributes before capture)
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
     graph = None
     try:
         if args.profile:
