@@ -122,6 +122,13 @@ int apb_dequant(const uint8_t* planes, int n_max, int64_t rows, int64_t cols,
                 int64_t padded_cols, int permuted, int k, const uint16_t* lut, void* w,
                 int w_dtype, int64_t ldw, void* stream);
 
+/* Dense path activation split (engine.py:343-354 at fp32 accuracy on tensor
+ * cores): out rows [0, m) = hi = fp16(x * s_r), rows [m, 2m) = lo =
+ * fp16(x * s_r - hi), inv_scale[r] = 1 / s_r with s_r the power of two that
+ * puts row r's max |x| in [2^14, 2^15).  Y = (hi.W^T + lo.W^T) * inv_scale. */
+int apb_split_hilo(const float* x, int64_t m, int64_t cols, int64_t ldx, uint16_t* out, int64_t ld,
+                   float* inv_scale, void* stream);
+
 /* Helper for the fp32-activation path: x fp32 [m][ldx_in] -> fp16 pairs
  * out [2m][ldx_out] with out[2i] = fp16(x[i]), out[2i+1] = fp16(x[i]-out[2i]).
  * Columns cols..ldx_out-1 are zero-filled.  With round_only = 1 it writes

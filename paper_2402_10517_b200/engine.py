@@ -304,7 +304,8 @@ def gemv(prep: PreparedLayer, x, cfg: GemvConfig, report: ExecutionReport | None
 def gemm(prep: PreparedLayer, x, cfg: GemvConfig, report: ExecutionReport | None = None):
     """Y = X @ dequant_k(W).T for a (M, in_features) batch (engine.py:312-354).
     M <= dense_threshold: quantized small-batch kernel (decode once, reuse the
-    weights across the batch); larger M: GPU dequantize + library GEMM."""
+    weights across the batch); larger M: GPU dequantize (exact fp16) + an
+    fp32-accurate tensor-core GEMM (hi/lo split activations)."""
     k = cfg.bit_width
     _check_bit_width(prep.layer, k)
     if not dev.is_tensor(x):
@@ -330,7 +331,8 @@ def gemm(prep: PreparedLayer, x, cfg: GemvConfig, report: ExecutionReport | None
     if shape[1] != t.cols:
         raise ShapeError(f"activation width {shape[1]} != in_features {t.cols}")
     torch = dev.require_cuda()
-    dense = _dequant_device(prep, k, APB_DTYPE_F32)
+    # the k-bit weights are fp16 table entries: dequantised to fp16 they are exact
+    dense = _dequant_device(prep, k, APB_DTYPE_F16)
     if report is not None:
         report.path_taken = "gemm-dense"
         report.planes_bytes_read += k * t.rows * t.padded_cols // 8
@@ -338,18 +340,29 @@ def gemm(prep: PreparedLayer, x, cfg: GemvConfig, report: ExecutionReport | None
     host = not dev.is_tensor(x)
     xd = dev.to_device(np.asarray(x)) if host else x.cuda()
     back = "numpy" if host else ("cuda" if x.is_cuda else "tensor")
-    if cfg.activations_fp16:
-        xd = xd.to(torch.float16)
-    xd = xd.to(torch.float32)
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False  # fp32 GEMM like the reference
-    try:
-        y = xd @ dense.T
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
+    y = _dense_tensor_core(torch, xd, dense, cfg.activations_fp16)
     if back == "numpy":
         return y.cpu().numpy()
     return y.cpu() if back == "tensor" else y
+
+
+def _dense_tensor_core(torch, x, w16, x_is_fp16: bool):
+    """Y = X @ W.T at fp32 accuracy on the tensor cores (the reference's dense
+    path is an fp32 GEMM, engine.py:343-354).  W is exact in fp16; X is split
+    into fp16 hi + lo halves after an exact power-of-two row scale (hi <= 2^15,
+    no overflow; X - hi is exact in fp32 and its fp16 rounding leaves ~2^-22
+    relative error; csrc/apb_dense.cu, one pass), and ONE fp16 x fp16 -> fp32
+    tensor-core GEMM over [hi; lo] accumulates both products in fp32."""
+    if x_is_fp16:
+        return torch.mm(x.to(torch.float16), w16.T, out_dtype=torch.float32)
+    x = x.to(torch.float32).contiguous()
+    m, c = x.shape
+    hilo = torch.empty((2 * m, c), dtype=torch.float16, device="cuda")
+    inv = torch.empty((m, 1), dtype=torch.float32, device="cuda")
+    check(load().apb_split_hilo(dev.ptr(x), m, c, c, dev.ptr(hilo), c, dev.ptr(inv), dev.stream_ptr()),
+          "apb_split_hilo")
+    yy = torch.mm(hilo, w16.T, out_dtype=torch.float32)
+    return yy[:m].add_(yy[m:]).mul_(inv)
 
 
 def _dequant_device(prep: PreparedLayer, k: int, dtype: int):

@@ -580,3 +580,33 @@ def test_norm_epilogues_producer_and_consumer(api):
         assert torch.allclose(c.y[0][0], s * plain, rtol=1e-5, atol=1e-5)
         gl = torch.nn.functional.silu(s * plain[0::2]) * (s * plain[1::2])
         assert torch.allclose(cg.y[0][0], gl, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("m", [64, 300])
+def test_dense_path_tensor_core_fp32_accuracy(api, m):
+    """gemm-dense (M > dense_threshold): exact fp16 dequantisation + hi/lo split
+    activations on the tensor cores must meet the reference's fp32 bar (1e-5
+    vs fp64), per row, including rows scaled by 1e4 / 1e-4 and an all-zero row."""
+    import torch
+
+    _, _, engine, _ = api
+    layer = _random_layer(api, 55, 1100, 4096)
+    prep = engine.prepare(layer)
+    rng = np.random.default_rng(m)
+    X = rng.standard_normal((m, 4096)).astype(np.float32)
+    X[1] *= 1e4
+    X[2] *= 1e-4
+    X[3] = 0.0
+    X[4, ::7] *= 300.0  # wide range inside one row
+    for k in (3, 6, 8):
+        rep = engine.ExecutionReport()
+        y = engine.gemm(prep, X, engine.GemvConfig(bit_width=k), report=rep)
+        assert rep.path_taken == "gemm-dense"
+        W = engine.dequantize(layer, k).astype(np.float64)
+        want = X.astype(np.float64) @ W.T
+        err = np.abs(y.astype(np.float64) - want).max(axis=1)
+        scale = np.maximum(np.abs(want).max(axis=1), 1e-30)
+        assert np.all(y[3] == 0.0)
+        rows = np.arange(m) != 3
+        assert (err[rows] / scale[rows]).max() < 1e-5, (k, (err[rows] / scale[rows]).max())
+        assert ora.rel_err(y, want) < TOL
