@@ -354,6 +354,7 @@ def run_ours(args):
         if not args.no_decode:
             result["decode_step"] = run_decode(torch)
             result["quantizer"] = run_quantizer(torch)
+            result["prefill_dense"] = run_prefill(torch, copies[0])
     if rank == 0:
         if world == 1:
             result["e2e"] = run_e2e_step(torch, plans, world)
@@ -410,6 +411,30 @@ def run_decode(torch, steps: int = 20):
     nbytes = codes.numel() + t.planes.numel()
     out["packer"] = {"shape": "11008x4096 codes -> 8 bitplanes (linear layout)", "ms": round(ms, 4),
                      "GBps": round(nbytes / (ms * 1e-3) / 1e9, 1)}
+    return out
+
+
+def run_prefill(torch, preps):
+    """engine.gemm above the dense threshold (prefill batches)
+    on the gate projection (11008x4096): exact fp16 dequantisation + hi/lo split
+    activations + one fp16 x fp16 -> fp32 tensor-core GEMM (fp32 accuracy)."""
+    from paper_2402_10517_b200 import engine
+
+    prep = preps[4]  # gate 11008x4096
+    out = {"layer": "gate 11008x4096", "k": 4, "per_M": {}}
+    for m in (64, 512, 2048):
+        x = torch.randn(m, 4096, device="cuda")
+        cfg = engine.GemvConfig(bit_width=4)
+        engine.gemm(prep, x, cfg)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(10):
+            engine.gemm(prep, x, cfg)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 10
+        out["per_M"][f"M{m}"] = {"ms": round(ms, 4), "TFLOPs": round(2 * m * 11008 * 4096 / (ms * 1e-3) / 1e12, 1)}
     return out
 
 
