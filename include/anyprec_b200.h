@@ -242,6 +242,20 @@ int64_t apb_quant_workspace(int rows, int n, int n_min, int n_max);
 int apb_quant_build(const double* weights, const double* sens, const int64_t* order, int rows, int n, int n_min,
                     int n_max, uint8_t* codes, uint16_t* tables, double* sse, uint8_t* level_codes,
                     void* workspace, int64_t workspace_bytes, void* stream);
+/* continue_upscale (quantizer.py:438-512): extend stored k0-bit codes (codes_in,
+ * [rows][n]) with fp16 table table_k0 ([rows][2^k0]) to new_n_max bits by
+ * splitting; codes / tables (k0+1..new_n_max concatenated) / sse
+ * ([new_n_max-k0][rows]) as in apb_quant_build; *bad |= 1 when some row's codes
+ * are not value-contiguous (the caller raises).  Workspace:
+ * apb_quant_workspace(rows, n, 2, new_n_max).
+ * apb_quant_sse_levels: np.sum(sens * (w - table_k[codes >> shift])**2, axis=1)
+ * in original column order (the record of the levels <= k0). */
+int apb_quant_continue(const double* weights, const double* sens, const int64_t* order, const uint8_t* codes_in,
+                       const uint16_t* table_k0, int rows, int n, int k0, int new_n_max, uint8_t* codes,
+                       uint16_t* tables, double* sse, int* bad, void* workspace, int64_t workspace_bytes,
+                       void* stream);
+int apb_quant_sse_levels(const double* weights, const double* sens, const uint8_t* codes, int shift,
+                         const uint16_t* table_k, int k, int rows, int n, double* sse, void* stream);
 
 #ifdef __cplusplus
 }

@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kThreads) seed_kernel(int rows, Ws W, void* ws
 // bounds area; writes the fp16 table, the SSE, optional level codes and, when
 // split != 0, the 2^(k+1) + 1 split bounds into the other slot.
 __global__ void __launch_bounds__(kThreads) level_kernel(int rows, Ws W, void* ws, int kbits, int cur, int seed,
-                                                         int split, uint16_t* __restrict__ table,
+                                                         int split, int only_split, uint16_t* __restrict__ table,
                                                          double* __restrict__ sse, uint8_t* __restrict__ codes_a,
                                                          uint8_t* __restrict__ codes_b,
                                                          const int64_t* __restrict__ order) {
@@ -359,140 +359,142 @@ __global__ void __launch_bounds__(kThreads) level_kernel(int rows, Ws W, void* w
     __shared__ double leaf[kMaxLeaves];
     for (int c = threadIdx.x; c <= m; c += kThreads) sb[c] = bounds[c];
     __syncthreads();
-    // interval means (clustering.py:60-83): reduceat sums of w, w*v, v
-    for (int c = threadIdx.x; c < m; c += kThreads) {
-        const int a = sb[c], len = sb[c + 1] - sb[c];
-        double mean = NAN;
-        if (len > 0) {
-            const double sum_w = reduceat_sum([&](int64_t i) { return sw[i]; }, a, len);
-            const double sum_wv = reduceat_sum([&](int64_t i) { return sw[i] * sv[i]; }, a, len);
-            if (sum_w > 0.0) {
-                mean = sum_wv / sum_w;
-            } else {
-                const double sum_v = reduceat_sum([&](int64_t i) { return sv[i]; }, a, len);
-                mean = sum_v / (double)len;
-            }
-        }
-        means[c] = mean;
-    }
-    __syncthreads();
-    // empty intervals (quantizer.py:244-259): seed -> copy the previous column;
-    // otherwise -> the parent's float64 centroid
-    if (seed) {
-        if (threadIdx.x == 0)
-            for (int c = 1; c < m; ++c)
-                if (isnan(means[c])) means[c] = means[c - 1];
-    } else {
-        for (int c = threadIdx.x; c < m; c += kThreads)
-            if (isnan(means[c])) means[c] = parents[c >> 1];
-    }
-    __syncthreads();
-    for (int c = threadIdx.x; c < m; c += kThreads) {
-        const __half h = __double2half(means[c]);
-        table[(int64_t)r * m + c] = __half_as_ushort(h);
-        t64[c] = (double)__half2float(h);
-        parents[c] = means[c];  // the next level's parents
-    }
-    __syncthreads();
-    // weighted SSE against the fp16 table (quantizer.py:272-278): np.sum over the
-    // row of (w * diff) * diff -- pairwise; leaves of <= 128 summed in parallel
-    {
-        auto code_of = [&](int64_t p) {
-            int lo = 0, hi = m - 1;  // last c with sb[c] <= p and sb[c+1] > p
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (sb[mid] <= p) lo = mid;
-                else hi = mid - 1;
-            }
-            return lo;
-        };
-        auto term = [&](int64_t p) {
-            const double d = sv[p] - t64[code_of(p)];
-            return sw[p] * d * d;
-        };
-        // enumerate the leaves of numpy's split tree (left to right)
-        __shared__ int64_t leaf_a[kMaxLeaves], leaf_n[kMaxLeaves];
-        __shared__ int n_leaves;
-        if (threadIdx.x == 0) {
-            int cnt = 0;
-            int64_t sa[40], sn[40];
-            int sp = 0;
-            sa[0] = 0;
-            sn[0] = n;
-            while (sp >= 0) {
-                const int64_t a = sa[sp], len = sn[sp];
-                --sp;
-                if (len <= kLeafMax || cnt >= kMaxLeaves) {
-                    leaf_a[cnt] = a;
-                    leaf_n[cnt] = len;
-                    ++cnt;
+    if (!only_split) {  // (continue_upscale's first step only splits the stored level)
+        // interval means (clustering.py:60-83): reduceat sums of w, w*v, v
+        for (int c = threadIdx.x; c < m; c += kThreads) {
+            const int a = sb[c], len = sb[c + 1] - sb[c];
+            double mean = NAN;
+            if (len > 0) {
+                const double sum_w = reduceat_sum([&](int64_t i) { return sw[i]; }, a, len);
+                const double sum_wv = reduceat_sum([&](int64_t i) { return sw[i] * sv[i]; }, a, len);
+                if (sum_w > 0.0) {
+                    mean = sum_wv / sum_w;
                 } else {
-                    int64_t n2 = len / 2;
-                    n2 -= n2 % 8;
-                    // push right first so the left is processed first
-                    ++sp;
-                    sa[sp] = a + n2;
-                    sn[sp] = len - n2;
-                    ++sp;
-                    sa[sp] = a;
-                    sn[sp] = n2;
+                    const double sum_v = reduceat_sum([&](int64_t i) { return sv[i]; }, a, len);
+                    mean = sum_v / (double)len;
                 }
             }
-            n_leaves = cnt;
+            means[c] = mean;
         }
         __syncthreads();
-        const bool small = n <= kMaxLeaves * kLeafMax / 2;  // every leaf of the split tree is >= 64
-        if (small) {
-            for (int l = threadIdx.x; l < n_leaves; l += kThreads) leaf[l] = pw_leaf(term, leaf_a[l], leaf_n[l]);
-            __syncthreads();
+        // empty intervals (quantizer.py:244-259): seed -> copy the previous column;
+        // otherwise -> the parent's float64 centroid
+        if (seed) {
+            if (threadIdx.x == 0)
+                for (int c = 1; c < m; ++c)
+                    if (isnan(means[c])) means[c] = means[c - 1];
+        } else {
+            for (int c = threadIdx.x; c < m; c += kThreads)
+                if (isnan(means[c])) means[c] = parents[c >> 1];
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < m; c += kThreads) {
+            const __half h = __double2half(means[c]);
+            table[(int64_t)r * m + c] = __half_as_ushort(h);
+            t64[c] = (double)__half2float(h);
+            parents[c] = means[c];  // the next level's parents
+        }
+        __syncthreads();
+        // weighted SSE against the fp16 table (quantizer.py:272-278): np.sum over the
+        // row of (w * diff) * diff -- pairwise; leaves of <= 128 summed in parallel
+        {
+            auto code_of = [&](int64_t p) {
+                int lo = 0, hi = m - 1;  // last c with sb[c] <= p and sb[c+1] > p
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (sb[mid] <= p) lo = mid;
+                    else hi = mid - 1;
+                }
+                return lo;
+            };
+            auto term = [&](int64_t p) {
+                const double d = sv[p] - t64[code_of(p)];
+                return sw[p] * d * d;
+            };
+            // enumerate the leaves of numpy's split tree (left to right)
+            __shared__ int64_t leaf_a[kMaxLeaves], leaf_n[kMaxLeaves];
+            __shared__ int n_leaves;
             if (threadIdx.x == 0) {
-                // recombine in the split tree's order
-                struct F2 {
-                    int64_t n;
-                    double left;
-                    int state;
-                } st[40];
-                int sp = 0, li = 0;
-                st[0] = {(int64_t)n, 0.0, 0};
-                double ret = 0.0;
-                while (true) {
-                    F2& fr = st[sp];
-                    if (fr.n <= kLeafMax) {
-                        ret = leaf[li++];
-                        if (sp == 0) break;
-                        --sp;
-                        continue;
-                    }
-                    int64_t n2 = fr.n / 2;
-                    n2 -= n2 % 8;
-                    if (fr.state == 0) {
-                        fr.state = 1;
-                        st[++sp] = {n2, 0.0, 0};
-                    } else if (fr.state == 1) {
-                        fr.left = ret;
-                        fr.state = 2;
-                        st[++sp] = {fr.n - n2, 0.0, 0};
+                int cnt = 0;
+                int64_t sa[40], sn[40];
+                int sp = 0;
+                sa[0] = 0;
+                sn[0] = n;
+                while (sp >= 0) {
+                    const int64_t a = sa[sp], len = sn[sp];
+                    --sp;
+                    if (len <= kLeafMax || cnt >= kMaxLeaves) {
+                        leaf_a[cnt] = a;
+                        leaf_n[cnt] = len;
+                        ++cnt;
                     } else {
-                        ret = fr.left + ret;
-                        if (sp == 0) break;
-                        --sp;
+                        int64_t n2 = len / 2;
+                        n2 -= n2 % 8;
+                        // push right first so the left is processed first
+                        ++sp;
+                        sa[sp] = a + n2;
+                        sn[sp] = len - n2;
+                        ++sp;
+                        sa[sp] = a;
+                        sn[sp] = n2;
                     }
                 }
-                sse[r] = ret;
+                n_leaves = cnt;
             }
-        } else if (threadIdx.x == 0) {
-            sse[r] = pairwise_sum(term, 0, n);
+            __syncthreads();
+            const bool small = n <= kMaxLeaves * kLeafMax / 2;  // every leaf of the split tree is >= 64
+            if (small) {
+                for (int l = threadIdx.x; l < n_leaves; l += kThreads) leaf[l] = pw_leaf(term, leaf_a[l], leaf_n[l]);
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    // recombine in the split tree's order
+                    struct F2 {
+                        int64_t n;
+                        double left;
+                        int state;
+                    } st[40];
+                    int sp = 0, li = 0;
+                    st[0] = {(int64_t)n, 0.0, 0};
+                    double ret = 0.0;
+                    while (true) {
+                        F2& fr = st[sp];
+                        if (fr.n <= kLeafMax) {
+                            ret = leaf[li++];
+                            if (sp == 0) break;
+                            --sp;
+                            continue;
+                        }
+                        int64_t n2 = fr.n / 2;
+                        n2 -= n2 % 8;
+                        if (fr.state == 0) {
+                            fr.state = 1;
+                            st[++sp] = {n2, 0.0, 0};
+                        } else if (fr.state == 1) {
+                            fr.left = ret;
+                            fr.state = 2;
+                            st[++sp] = {fr.n - n2, 0.0, 0};
+                        } else {
+                            ret = fr.left + ret;
+                            if (sp == 0) break;
+                            --sp;
+                        }
+                    }
+                    sse[r] = ret;
+                }
+            } else if (threadIdx.x == 0) {
+                sse[r] = pairwise_sum(term, 0, n);
+            }
         }
-    }
-    // codes of this level (scattered back through the sort order)
-    if (codes_a || codes_b) {
-        const int64_t* orr = order + (int64_t)r * n;
-        for (int c = warp; c < m; c += kWarps)
-            for (int p = sb[c] + lane; p < sb[c + 1]; p += 32) {
-                const int64_t o = (int64_t)r * n + orr[p];
-                if (codes_a) codes_a[o] = (uint8_t)c;
-                if (codes_b) codes_b[o] = (uint8_t)c;
-            }
+        // codes of this level (scattered back through the sort order)
+        if (codes_a || codes_b) {
+            const int64_t* orr = order + (int64_t)r * n;
+            for (int c = warp; c < m; c += kWarps)
+                for (int p = sb[c] + lane; p < sb[c + 1]; p += 32) {
+                    const int64_t o = (int64_t)r * n + orr[p];
+                    if (codes_a) codes_a[o] = (uint8_t)c;
+                    if (codes_b) codes_b[o] = (uint8_t)c;
+                }
+        }
     }
     if (!split) return;
     // 2-means split of every interval (clustering.py:252-302): warp per interval
@@ -537,6 +539,63 @@ __global__ void __launch_bounds__(kThreads) level_kernel(int rows, Ws W, void* w
     }
 }
 
+// continue_upscale (quantizer.py:469-484): the stored k0-bit codes in sorted
+// order must be non-decreasing (value-contiguous clusters); their counts give
+// the k0-level interval bounds (slot 0), and the fp16 table of k0 (as float64)
+// is the parent of the first split (quantizer.py:484).
+__global__ void __launch_bounds__(kThreads) bounds_from_codes_kernel(int rows, Ws W, void* ws,
+                                                                     const uint8_t* __restrict__ codes, int k0,
+                                                                     const int64_t* __restrict__ order,
+                                                                     const uint16_t* __restrict__ table,
+                                                                     int* __restrict__ bad) {
+    const int r = blockIdx.x;
+    if (r >= rows) return;
+    const int n = W.n, m = 1 << k0;
+    __shared__ int cnt[kMaxIntervals];
+    for (int c = threadIdx.x; c < m; c += kThreads) cnt[c] = 0;
+    __syncthreads();
+    const uint8_t* cr = codes + (int64_t)r * n;
+    const int64_t* orr = order + (int64_t)r * n;
+    bool ok = true;
+    for (int p = threadIdx.x; p < n; p += kThreads) {
+        const int c = cr[orr[p]];
+        if (c >= m || (p > 0 && c < cr[orr[p - 1]])) ok = false;
+        else atomicAdd(&cnt[c], 1);
+    }
+    if (!ok) atomicOr(bad, 1);
+    __syncthreads();
+    int* bounds = slice<int>(ws, W, r, W.off_bounds);  // slot 0
+    double* parents = slice<double>(ws, W, r, W.off_parents);
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        bounds[0] = 0;
+        for (int c = 0; c < m; ++c) {
+            acc += cnt[c];
+            bounds[c + 1] = acc;
+        }
+    }
+    for (int c = threadIdx.x; c < m; c += kThreads)
+        parents[c] = (double)__half2float(__ushort_as_half(table[(int64_t)r * m + c]));
+}
+
+// continue_upscale's error record of the EXISTING levels (quantizer.py:499-503):
+// np.sum(s * (w - table_k[codes >> shift]) ** 2, axis=1) over the row in its
+// original column order -- numpy's pairwise summation, one thread per row.
+__global__ void sse_levels_kernel(const double* __restrict__ w, const double* __restrict__ s,
+                                  const uint8_t* __restrict__ codes, int shift, const uint16_t* __restrict__ table,
+                                  int k, int rows, int n, double* __restrict__ sse) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const int64_t base = (int64_t)r * n;
+    const uint16_t* tr = table + ((int64_t)r << k);
+    auto term = [&](int64_t i) {
+        const double deq = (double)__half2float(__ushort_as_half(tr[codes[base + i] >> shift]));
+        const double d = w[base + i] - deq;
+        return s[base + i] * (d * d);
+    };
+    sse[r] = pairwise_sum(term, 0, n);
+}
+
 int finish() { return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA; }
 
 }  // namespace
@@ -562,11 +621,50 @@ extern "C" int apb_quant_build(const double* weights, const double* sens, const 
     for (int k = n_min; k <= n_max; ++k) {
         const int last = k == n_max;
         uint8_t* lc = level_codes ? level_codes + (int64_t)(k - n_min) * rows * n : nullptr;
-        level_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, k, cur, k == n_min, !last, tables + toff,
+        level_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, k, cur, k == n_min, !last, 0, tables + toff,
                                                  sse + (int64_t)(k - n_min) * rows, lc, last ? codes : nullptr,
                                                  order);
         toff += (int64_t)rows << k;
         cur ^= 1;
     }
+    return finish();
+}
+
+extern "C" int apb_quant_continue(const double* weights, const double* sens, const int64_t* order,
+                                  const uint8_t* codes_in, const uint16_t* table_k0, int rows, int n, int k0,
+                                  int new_n_max, uint8_t* codes, uint16_t* tables, double* sse, int* bad,
+                                  void* workspace, int64_t workspace_bytes, void* stream) {
+    if (!weights || !sens || !order || !codes_in || !table_k0 || !codes || !tables || !sse || !bad || !workspace)
+        return APB_ERR_PARAM;
+    if (rows <= 0 || n <= 0) return APB_ERR_SHAPE;
+    if (k0 < 2 || new_n_max <= k0 || new_n_max > kMaxLevelBits) return APB_ERR_PARAM;
+    const int64_t need = apb_quant_workspace(rows, n, 2, new_n_max);
+    if (workspace_bytes < need || ((uintptr_t)workspace & 15)) return APB_ERR_PARAM;
+    cudaStream_t st = (cudaStream_t)stream;
+    const Ws W(n, 1 << 2, new_n_max);  // no DP here
+    prefix_kernel<<<(rows + 127) / 128, 128, 0, st>>>(weights, sens, order, rows, W, workspace);
+    bounds_from_codes_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, codes_in, k0, order, table_k0, bad);
+    level_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, k0, 0, 0, 1, 1, nullptr, nullptr, nullptr, nullptr,
+                                             order);
+    int cur = 1;
+    int64_t toff = 0;
+    for (int k = k0 + 1; k <= new_n_max; ++k) {
+        const int last = k == new_n_max;
+        level_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, k, cur, 0, !last, 0, tables + toff,
+                                                 sse + (int64_t)(k - k0 - 1) * rows, nullptr, last ? codes : nullptr,
+                                                 order);
+        toff += (int64_t)rows << k;
+        cur ^= 1;
+    }
+    return finish();
+}
+
+extern "C" int apb_quant_sse_levels(const double* weights, const double* sens, const uint8_t* codes, int shift,
+                                    const uint16_t* table_k, int k, int rows, int n, double* sse, void* stream) {
+    if (!weights || !sens || !codes || !table_k || !sse) return APB_ERR_PARAM;
+    if (rows <= 0 || n <= 0) return APB_ERR_SHAPE;
+    if (k < 1 || k > kMaxLevelBits || shift < 0 || shift > 7) return APB_ERR_PARAM;
+    sse_levels_kernel<<<(rows + 127) / 128, 128, 0, (cudaStream_t)stream>>>(weights, sens, codes, shift, table_k, k,
+                                                                            rows, n, sse);
     return finish();
 }

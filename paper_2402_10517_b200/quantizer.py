@@ -129,3 +129,73 @@ def build_any_precision(weights, sens, n_min: int, n_max: int, *, record_levels:
     if record_levels:
         layer.level_codes = {k: conv(lvl[k - n_min]) for k in range(n_min, n_max + 1)}
     return layer
+
+
+def continue_upscale(weights, sens, layer, new_n_max: int, *, row_block: int | None = None,
+                     as_numpy: bool = True):
+    """Extend an existing layer to a higher parent bit-width (quantizer.py:438-512):
+    the stored n_max-bit codes define the clusters that keep splitting (codes
+    must be value-contiguous in each row's sorted order, else ParameterError),
+    the fp16 table of the old n_max is the parent of the first split, and the
+    error record of the existing levels is recomputed against the new codes."""
+    torch = dev.require_cuda()
+    from ._lib import check, load
+
+    w = _to_device_f64(torch, weights).contiguous()
+    if tuple(w.shape) != tuple(layer.shape):
+        raise ShapeError(f"weights shape {tuple(w.shape)} != layer shape {tuple(layer.shape)}")
+    if not layer.n_max < new_n_max <= MAX_BITS:
+        raise ParameterError(f"new parent bit-width {new_n_max} must be in ({layer.n_max}, {MAX_BITS}]")
+    s = _coerce_sensitivity(torch, w, sens)
+    rows, n = w.shape
+    k0 = layer.n_max
+    codes_in = layer.codes if dev.is_tensor(layer.codes) else torch.from_numpy(np.ascontiguousarray(layer.codes))
+    codes_in = codes_in.to(device="cuda", dtype=torch.uint8).contiguous()
+    t0 = layer.centroid_tables[k0]
+    t0 = (t0 if dev.is_tensor(t0) else torch.from_numpy(np.ascontiguousarray(t0, dtype=np.float16)))
+    t0 = t0.to(device="cuda", dtype=torch.float16).contiguous()
+
+    lib = load()
+    per_row = lib.apb_quant_workspace(1, n, 2, new_n_max)
+    block = max(1, min(rows, _WORKSPACE_BUDGET // max(per_row, 1)))
+    if row_block is not None:
+        block = max(1, min(block, int(row_block)))
+    new_levels = new_n_max - k0
+    codes = torch.empty(rows, n, dtype=torch.uint8, device="cuda")
+    tables = {k: torch.empty(rows, 1 << k, dtype=torch.float16, device="cuda") for k in range(k0 + 1, new_n_max + 1)}
+    sse = torch.empty(new_levels, rows, dtype=torch.float64, device="cuda")
+    ws = torch.empty(lib.apb_quant_workspace(block, n, 2, new_n_max), dtype=torch.uint8, device="cuda")
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st, P = dev.stream_ptr(), dev.ptr
+    for lo in range(0, rows, block):
+        hi = min(rows, lo + block)
+        nb = hi - lo
+        order = torch.sort(w[lo:hi] + 0.0, dim=1, stable=True).indices.contiguous()
+        tb = torch.empty(sum(nb << k for k in range(k0 + 1, new_n_max + 1)), dtype=torch.float16, device="cuda")
+        sseb = torch.empty(new_levels, nb, dtype=torch.float64, device="cuda")
+        check(lib.apb_quant_continue(P(w[lo:hi]), P(s[lo:hi]), P(order), P(codes_in[lo:hi]), P(t0[lo:hi]), nb, n,
+                                     k0, new_n_max, P(codes[lo:hi]), P(tb), P(sseb), P(bad), P(ws), ws.numel(),
+                                     st), "apb_quant_continue")
+        if int(bad.item()):
+            raise ParameterError("stored codes are not value-contiguous; re-quantize from weights instead")
+        off = 0
+        for k in range(k0 + 1, new_n_max + 1):
+            tables[k][lo:hi] = tb[off:off + (nb << k)].view(nb, 1 << k)
+            off += nb << k
+        sse[:, lo:hi] = sseb
+    # the existing levels: old tables, error recomputed against the new codes
+    all_tables, all_sse = {}, {}
+    for k in range(layer.n_min, k0 + 1):
+        tk = layer.centroid_tables[k]
+        tk = (tk if dev.is_tensor(tk) else torch.from_numpy(np.ascontiguousarray(tk, dtype=np.float16)))
+        tk = tk.to(device="cuda", dtype=torch.float16).contiguous()
+        out = torch.empty(rows, dtype=torch.float64, device="cuda")
+        check(lib.apb_quant_sse_levels(P(w), P(s), P(codes), new_n_max - k, P(tk), k, rows, n, P(out), st),
+              "apb_quant_sse_levels")
+        all_tables[k], all_sse[k] = tk, out
+    for k in range(k0 + 1, new_n_max + 1):
+        all_tables[k], all_sse[k] = tables[k], sse[k - k0 - 1]
+    conv = (lambda t: t.cpu().numpy()) if as_numpy else (lambda t: t)
+    return AnyPrecisionLayer(n_min=layer.n_min, n_max=new_n_max, codes=conv(codes),
+                             centroid_tables={k: conv(t) for k, t in all_tables.items()}, shape=(rows, n),
+                             channel_sse={k: conv(t) for k, t in all_sse.items()})

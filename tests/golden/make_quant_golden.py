@@ -10,7 +10,8 @@ for every k, float64 channel_sse for every k, level codes).  The cases cover
 random rows with zero-sensitivity entries and a dead (all-zero) row,
 low-distinct rows (k_eff < 2^n_min, padded tables, unsplittable clusters),
 duplicates, -0.0 / +0.0 ties, n_min = 2, and a row wider than 8192 (deep
-pairwise-summation tree).  Nothing at test or bench time reads /root/reference.
+pairwise-summation tree); plus continue_upscale of a 3..5-bit layer to 8 bits
+("cont/*") and its error message for codes that are not value-contiguous.  Nothing at test or bench time reads /root/reference.
 """
 
 from __future__ import annotations
@@ -69,6 +70,31 @@ def main():
             out[f"{name}/sse{k}"] = layer.channel_sse[k]
             out[f"{name}/level{k}"] = layer.level_codes[k]
     out["cases"] = np.array(names)
+    # continue_upscale (quantizer.py:438-512): a 3..5-bit layer extended to 8 bits
+    from anyprec.quantizer import continue_upscale  # noqa: E402
+    from anyprec.errors import ParameterError  # noqa: E402
+
+    rng = np.random.default_rng(77)
+    w = rng.standard_normal((9, 640))
+    s = rng.random((9, 640))
+    s[2] = 0.0  # dead row -> uniform
+    base = build_any_precision(w, s, 3, 5)
+    ext = continue_upscale(w, s, base, 8)
+    out["cont/weights"], out["cont/sens"] = w, s
+    out["cont/base_codes"] = base.codes
+    for k in range(3, 6):
+        out[f"cont/base_table{k}"] = base.centroid_tables[k]
+    out["cont/codes"] = ext.codes
+    for k in range(3, 9):
+        out[f"cont/table{k}"] = ext.centroid_tables[k]
+        out[f"cont/sse{k}"] = ext.channel_sse[k]
+    out["cont/bad_codes"] = rng.integers(0, 32, size=(9, 640), dtype=np.uint8)
+    try:
+        continue_upscale(w, s, type(base)(n_min=3, n_max=5, codes=out["cont/bad_codes"],
+                                          centroid_tables=base.centroid_tables, shape=base.shape), 8)
+        out["cont/bad_msg"] = np.array("")
+    except ParameterError as e:
+        out["cont/bad_msg"] = np.array(str(e))
     np.savez_compressed(os.path.join(OUT, "quant_golden.npz"), **out)
     print("wrote", len(names), "cases")
 

@@ -102,3 +102,31 @@ def test_quantizer_validation_matches_reference():
         build_any_precision(w, np.ones((4, 15)), 3, 4)
     with pytest.raises(ParameterError, match="non-negative"):
         build_any_precision(w, -np.ones((4, 16)), 3, 4)
+
+
+def test_continue_upscale_bit_exact_vs_reference():
+    """continue_upscale (quantizer.py:438-512): 3..5-bit layer (the reference's
+    own) extended to 8 bits -- codes, every table and every level's SSE (the
+    existing levels recomputed in original column order) bit-identical; codes
+    that are not value-contiguous raise the reference's ParameterError."""
+    from paper_2402_10517_b200 import AnyPrecisionLayer
+    from paper_2402_10517_b200.errors import ParameterError
+    from paper_2402_10517_b200.quantizer import continue_upscale
+
+    z = np.load(GOLDEN)
+    w, s = z["cont/weights"], z["cont/sens"]
+    base = AnyPrecisionLayer(n_min=3, n_max=5, codes=z["cont/base_codes"],
+                             centroid_tables={k: z[f"cont/base_table{k}"] for k in range(3, 6)}, shape=w.shape)
+    ext = continue_upscale(w, s, base, 8)
+    np.testing.assert_array_equal(ext.codes, z["cont/codes"])
+    for k in range(3, 9):
+        np.testing.assert_array_equal(ext.centroid_tables[k].view(np.uint16), z[f"cont/table{k}"].view(np.uint16),
+                                      err_msg=f"table k={k}")
+        np.testing.assert_array_equal(ext.channel_sse[k].view(np.uint64), z[f"cont/sse{k}"].view(np.uint64),
+                                      err_msg=f"sse k={k}")
+    bad = AnyPrecisionLayer(n_min=3, n_max=5, codes=z["cont/bad_codes"], centroid_tables=base.centroid_tables,
+                            shape=w.shape)
+    with pytest.raises(ParameterError, match=str(z["cont/bad_msg"])):
+        continue_upscale(w, s, bad, 8)
+    with pytest.raises(ParameterError):
+        continue_upscale(w, s, base, 5)
