@@ -72,7 +72,7 @@ static Layer make_layer(int64_t R, int64_t C, int ncopy, uint32_t seed, int M) {
 static int64_t lut_off(int64_t R, int k) { int64_t o = 0; for (int b = 2; b < k; ++b) o += R << b; return o; }
 
 int main(int argc, char** argv) {
-    int ncopy = 4, reps = 20;
+    int ncopy = getenv("KB_NCOPY") ? atoi(getenv("KB_NCOPY")) : 4, reps = 20;  // KB_NCOPY=1: L2-resident weights
     std::string only = argc > 1 ? argv[1] : "";
     int konly = argc > 2 ? atoi(argv[2]) : 0;   // 0 = k 3..8
     if (argc > 3) reps = atoi(argv[3]);
@@ -86,7 +86,7 @@ int main(int argc, char** argv) {
     std::vector<double> h_ref(8 * 28672); std::vector<float> h_y(8 * 28672);
     for (auto& sh : shapes) {
         if (!only.empty() && only.find(sh.n) == std::string::npos && only != "all") continue;
-        int nc = sh.R * sh.C > 100000000 ? 2 : ncopy;
+        int nc = sh.R * sh.C > 100000000 && ncopy > 2 ? 2 : ncopy;
         Layer L = make_layer(sh.R, sh.C, nc, 1234, M);
         CK(cudaDeviceSynchronize());
         printf("%-11s", sh.n);
