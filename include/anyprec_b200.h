@@ -116,6 +116,21 @@ int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, const int* n_
                      const int64_t* ldx, int x_split, void* const* y, int y_dtype,
                      const int64_t* ldy, int flags, void* stream);
 
+/* Caller-owned launch plan for repeated calls with the same layers / shapes:
+ * apb_gemv_plan_create validates and prepares everything of an
+ * apb_gemv_grouped call except the activation / output pointers (tensor maps,
+ * partition, launch shape) and returns an opaque heap object (NULL when the
+ * call is not served by the TMA kernel, e.g. m_x > 8: use apb_gemv_grouped).
+ * apb_gemv_plan_launch launches it with new x / y pointers (NULL: keep the
+ * previous ones; same shapes, x 16-byte aligned).  A plan is not thread-safe;
+ * destroy it with apb_gemv_plan_destroy. */
+void* apb_gemv_plan_create(int n_problems, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
+                           const int64_t* cols, const int64_t* padded_cols, int k, const uint16_t* const* lut,
+                           const uint16_t* const* x, int m_x, const int64_t* ldx, int x_split, void* const* y,
+                           int y_dtype, const int64_t* ldy, int flags);
+int apb_gemv_plan_launch(void* plan, const uint16_t* const* x, void* const* y, void* stream);
+void apb_gemv_plan_destroy(void* plan);
+
 /* engine.py:357-362 dequantize, from the top-k planes: w [rows][ldw] of
  * w_dtype (fp16 is exact: the values ARE fp16 table entries). */
 int apb_dequant(const uint8_t* planes, int n_max, int64_t rows, int64_t cols,

@@ -1154,6 +1154,37 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
     return APB_OK;
 }
 
+extern "C" void* apb7_plan_create(int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
+                                  const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
+                                  const uint16_t* const* x, int m_x, const int64_t* ldx, int x_split, void* const* y,
+                                  int y_dtype, const int64_t* ldy, int flags);
+
+// Caller-owned launch plan (apb_gemv_plan_create / _launch / _destroy): the
+// arguments of apb_gemv_grouped validated and prepared once; NULL when the call
+// is not served by the TMA kernel (use apb_gemv_grouped then).
+extern "C" void* apb_gemv_plan_create(int n_problems, const uint8_t* const* planes, const int* n_max,
+                                      const int64_t* rows, const int64_t* cols, const int64_t* padded_cols, int k,
+                                      const uint16_t* const* lut, const uint16_t* const* x, int m_x,
+                                      const int64_t* ldx, int x_split, void* const* y, int y_dtype,
+                                      const int64_t* ldy, int flags) {
+    if (n_problems < 1 || n_problems > 16 || k < 3 || k > 8) return nullptr;
+    if (y_dtype != APB_DTYPE_F32 && y_dtype != APB_DTYPE_F16) return nullptr;
+    if (m_x < 1 || m_x > 8 || (x_split && (m_x & 1))) return nullptr;
+    const bool glu = (flags & APB_FLAG_GLU) != 0;
+    for (int i = 0; i < n_problems; ++i) {
+        if (rows[i] <= 0 || cols[i] <= 0 || (glu && (rows[i] & 1))) return nullptr;
+        if (padded_cols[i] != apb_pad_columns(cols[i])) return nullptr;
+        if (k > n_max[i] || n_max[i] > 8) return nullptr;
+        if (ldx[i] < cols[i] || (ldx[i] % 8) != 0) return nullptr;
+        if (!planes[i] || !lut[i] || !x[i] || !y[i]) return nullptr;
+        if (((uintptr_t)x[i] & 15) != 0 || ((uintptr_t)planes[i] & 15) != 0 || ((uintptr_t)lut[i] & 15) != 0)
+            return nullptr;
+        if (ldy[i] < (glu ? rows[i] / 2 : rows[i])) return nullptr;
+    }
+    return apb7_plan_create(n_problems, planes, n_max, rows, cols, padded_cols, k, lut, x, m_x, ldx, x_split, y,
+                            y_dtype, ldy, flags);
+}
+
 // Row-sharded GEMV with the all-gather fused into the epilogue:
 // the grouped GEMV of this rank's row slab, every y value also stored into the
 // same place of each peer's output (y_peers[i * n_peers + j]: problem i's y as

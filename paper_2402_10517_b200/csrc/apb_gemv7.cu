@@ -1135,6 +1135,15 @@ extern "C" int apb7_read_timeline(unsigned long long* host, int n) {
 extern "C" void apb7_timeline_reset(void) { g_tl_host_launch = 0; }
 #endif
 
+namespace apb7 {
+int apb7_build(Launch7& L, int& nb, int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
+               const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
+               const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split, void* const* y,
+               int y_dtype, const int64_t* ldy, int64_t y_off, int flags, int n_peers, void* const* y_peers,
+               uint32_t* const* peer_flags, const apb_norm_epilogue* norm);
+int apb7_dispatch(Launch7& L, int k, int nb, int flags, cudaStream_t s);
+}  // namespace apb7
+
 extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
                              const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
                              const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split,
@@ -1148,10 +1157,26 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     }();
     // batch rows: <= 2 row-copy mapping (x in smem), 3..8 batch-in-N mapping
     // (measured faster than the two-batch-pair row-copy path from 3 rows up)
-    if (disabled || k < 3 || k > 8 || m_x > 8 || n > kMaxProb || n_peers > kMaxPeers - 1) return -1;
+    if (disabled) return -1;
+    static thread_local Launch7 L;  // ~7 KB: kept off the stack
+    int nb = 0;
+    const int rc = apb7::apb7_build(L, nb, n, planes, n_max, rows, cols, padded, k, lut, x, m_x, ldx, x_off, x_split, y,
+                                    y_dtype, ldy, y_off, flags, n_peers, y_peers, peer_flags, norm);
+    if (rc != 0) return rc;
+    return apb7::apb7_dispatch(L, k, nb, flags, (cudaStream_t)stream);
+}
+
+namespace apb7 {
+// Launch7 of a call (tensor maps encoded, partition fixed); -1 when this kernel
+// does not apply.  No argument validation beyond that (the callers validate).
+int apb7_build(Launch7& L, int& nb, int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
+               const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
+               const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split, void* const* y,
+               int y_dtype, const int64_t* ldy, int64_t y_off, int flags, int n_peers, void* const* y_peers,
+               uint32_t* const* peer_flags, const apb_norm_epilogue* norm) {
+    if (k < 3 || k > 8 || m_x > 8 || n > kMaxProb || n_peers > kMaxPeers - 1) return -1;
     for (int i = 0; i < n; ++i)
         if (padded[i] > kMaxCols) return -1;
-    static thread_local Launch7 L;  // ~5 KB: kept off the stack
     std::memset(&L, 0, sizeof(L));
     L.n_prob = n;
     L.m_x = m_x;
@@ -1212,12 +1237,15 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
 #ifdef APB_TIMELINE
     L.tl_launch = g_tl_host_launch++;
 #endif
-    cudaStream_t s = (cudaStream_t)stream;
 #ifndef APB7_NB2_MAX
 #define APB7_NB2_MAX 2
 #endif
-    const int nb = m_x <= 2 ? 1 : (m_x <= APB7_NB2_MAX ? 2 : 4);
+    nb = m_x <= 2 ? 1 : (m_x <= APB7_NB2_MAX ? 2 : 4);
     if (nb > 1) L.xs_bytes = 0;
+    return 0;
+}
+
+int apb7_dispatch(Launch7& L, int k, int nb, int flags, cudaStream_t s) {
     const bool epi = L.glu || L.norm_mode || L.n_peers >= 0;
     switch (k * 8 + nb) {
 #define APB7_L(K, NB, CPS) (epi ? launch<K, NB, CPS, true>(L, flags, s) : launch<K, NB, CPS, false>(L, flags, s))
@@ -1236,3 +1264,51 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     }
     return -1;
 }
+}  // namespace apb7
+
+// ---- caller-owned launch plans: everything but the activation / output
+// pointers prepared once (validation, tensor-map encoding, partition) --------
+struct ApbGemvPlan7 {
+    apb7::Launch7 L;
+    int k, nb, flags, n;
+    int64_t esz;
+};
+
+extern "C" void* apb7_plan_create(int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
+                                  const int64_t* cols, const int64_t* padded, int k, const uint16_t* const* lut,
+                                  const uint16_t* const* x, int m_x, const int64_t* ldx, int x_split, void* const* y,
+                                  int y_dtype, const int64_t* ldy, int flags) {
+    auto* p = new (std::nothrow) ApbGemvPlan7;
+    if (!p) return nullptr;
+    int nb = 0;
+    if (apb7::apb7_build(p->L, nb, n, planes, n_max, rows, cols, padded, k, lut, x, m_x, ldx, 0, x_split, y, y_dtype,
+                         ldy, 0, flags, 0, nullptr, nullptr, nullptr) != 0) {
+        delete p;
+        return nullptr;
+    }
+    p->k = k;
+    p->nb = nb;
+    p->flags = flags;
+    p->n = n;
+    p->esz = y_dtype == APB_DTYPE_F16 ? 2 : 4;
+    return p;
+}
+
+extern "C" int apb_gemv_plan_launch(void* plan, const uint16_t* const* x, void* const* y, void* stream) {
+    auto* p = static_cast<ApbGemvPlan7*>(plan);
+    if (!p) return APB_ERR_PARAM;
+    for (int i = 0; i < p->n; ++i) {
+        if (x) {
+            if (!x[i] || ((uintptr_t)x[i] & 15)) return APB_ERR_PARAM;
+            p->L.prob[i].x = x[i];
+        }
+        if (y) {
+            if (!y[i]) return APB_ERR_PARAM;
+            p->L.prob[i].y = y[i];
+        }
+    }
+    return apb7::apb7_dispatch(p->L, p->k, p->nb, p->flags, (cudaStream_t)stream);
+}
+
+extern "C" void apb_gemv_plan_destroy(void* plan) { delete static_cast<ApbGemvPlan7*>(plan); }
+

@@ -15,12 +15,14 @@ same MMA, so the default path stays within ~1e-6 of the fp32 reference.
 
 from __future__ import annotations
 
+import ctypes
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _device as dev
-from ._lib import APB_DTYPE_F16, APB_DTYPE_F32, check, load
+from ._lib import APB_DTYPE_F16, APB_DTYPE_F32, check, int64_array, int_array, load, ptr_array
 from .bitplane import (
     LANES,
     LAYOUT_PERMUTED,
@@ -171,6 +173,18 @@ class PreparedLayer:
                 raise ShapeError(f"centroid table {k} has shape {tuple(t16.shape)}")
             self.tables16[k] = t16
         self._merged = None
+        self._tls = threading.local()  # per-thread launch plans of the per-call API
+
+    def _call_plan(self, k: int, m_x: int, split: int):
+        """The cached launch plan of this (k, activation rows, split) for the
+        calling thread (plans hold mutable pointers: never shared across threads)."""
+        plans = getattr(self._tls, "plans", None)
+        if plans is None:
+            plans = self._tls.plans = {}
+        key = (k, m_x, split)
+        if key not in plans:
+            plans[key] = _CallPlan(self, k, m_x, split)
+        return plans[key]
 
     @property
     def planes(self):
@@ -243,12 +257,91 @@ def _stage_x(x, cols: int, fp16: bool):
     return dev.to_device(h), 2 * m, ldx, 1, "numpy"
 
 
+class _CallPlan:
+    """One (layer, k, activation rows) launch of the per-call API: a caller-owned
+    C launch plan (apb_gemv_plan_create: validation, tensor maps and partition
+    done once) plus device and pinned host staging buffers reused across calls.
+    ``handle`` is None when the TMA kernel does not serve the shape (k = 2,
+    m_x > 8, > 64K columns): the caller then uses apb_gemv directly."""
+
+    def __init__(self, prep: PreparedLayer, k: int, m_x: int, split: int):
+        torch = dev.torch()
+        t = prep.tensor
+        self.m_x, self.split, self.ldx = m_x, split, _ldx(t.cols)
+        self.m_out = m_x // 2 if split else m_x
+        self.x = torch.zeros((m_x, self.ldx), dtype=torch.float16, device="cuda")
+        self.y = torch.empty((self.m_out, t.rows), dtype=torch.float32, device="cuda")
+        self.x_pin = torch.zeros((m_x, self.ldx), dtype=torch.float16, pin_memory=True)
+        self.y_pin = torch.empty((self.m_out, t.rows), dtype=torch.float32, pin_memory=True)
+        self._lib = load()
+        PP = lambda a: ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))  # noqa: E731
+        self._keep = (ptr_array([dev.ptr(t.planes)]), int_array([t.n_max]), int64_array([t.rows]),
+                      int64_array([t.cols]), int64_array([t.padded_cols]), ptr_array([dev.ptr(prep.tables16[k])]),
+                      ptr_array([dev.ptr(self.x)]), int64_array([self.ldx]), ptr_array([dev.ptr(self.y)]),
+                      int64_array([t.rows]))
+        pl, nm, rw, cl, pd, lt, xp, lx, yp, ly = self._keep
+        h = self._lib.apb_gemv_plan_create(1, PP(pl), nm, rw, cl, pd, k, PP(lt), PP(xp), m_x, lx, split, PP(yp),
+                                           APB_DTYPE_F32, ly, 0)
+        self.handle = h or None
+        self._xa = (ctypes.c_void_p * 1)()
+        self._ya = (ctypes.c_void_p * 1)()
+
+    def launch(self, xptr=None, yptr=None):
+        xa = ya = None
+        if xptr is not None:
+            self._xa[0] = xptr
+            xa = ctypes.cast(self._xa, ctypes.POINTER(ctypes.c_void_p))
+        if yptr is not None:
+            self._ya[0] = yptr
+            ya = ctypes.cast(self._ya, ctypes.POINTER(ctypes.c_void_p))
+        check(self._lib.apb_gemv_plan_launch(self.handle, xa, ya, dev.stream_ptr()), "apb_gemv_plan_launch")
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            self._lib.apb_gemv_plan_destroy(self.handle)
+            self.handle = None
+
+
+def _host_rows(x, m: int, fp16: bool):
+    """Host activation block -> its staged fp16 rows (m_x, split) as numpy."""
+    x = x.numpy() if dev.is_tensor(x) else np.asarray(x)
+    if fp16 or x.dtype == np.float16:
+        return x.astype(np.float16), m, 0
+    x32 = x.astype(np.float32)
+    hi = x32.astype(np.float16)
+    lo = (x32 - hi.astype(np.float32)).astype(np.float16)
+    h = np.empty((2 * m, x.shape[1]), dtype=np.float16)
+    h[0::2], h[1::2] = hi, lo
+    return h, 2 * m, 1
+
+
 def _quantized(prep: PreparedLayer, x2, k: int, fp16: bool):
     """The GPU quantized path for a (m, cols) activation block."""
     torch = dev.require_cuda()
     t = prep.tensor
+    m = _shape_of(x2)[0]
+    host = not (dev.is_tensor(x2) and x2.is_cuda)
+    if host:
+        # host activations: staged in this thread's pinned buffer, one async H2D,
+        # the prepared launch, one D2H into pinned memory, one stream sync
+        rows16, m_x, split = _host_rows(x2, m, fp16)
+        plan = prep._call_plan(k, m_x, split)
+        if plan.handle is not None:
+            plan.x_pin.numpy()[:, :t.cols] = rows16
+            plan.x.copy_(plan.x_pin, non_blocking=True)
+            plan.launch(dev.ptr(plan.x), dev.ptr(plan.y))  # (a device call may have re-pointed the plan)
+            plan.y_pin.copy_(plan.y, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            out = plan.y_pin.numpy().copy()
+            return out if not dev.is_tensor(x2) else torch.from_numpy(out)
     xdev, m_x, ldx, split, kind = _stage_x(x2, t.cols, fp16)
     m_out = m_x // 2 if split else m_x
+    if not host:
+        plan = prep._call_plan(k, m_x, split)
+        if plan.handle is not None and ldx == plan.ldx:
+            y = torch.empty((m_out, t.rows), dtype=torch.float32, device=xdev.device)
+            plan.launch(dev.ptr(xdev), dev.ptr(y))
+            return y
     y = torch.empty((m_out, t.rows), dtype=torch.float32, device=xdev.device)
     check(
         load().apb_gemv(dev.ptr(t.planes), t.n_max, t.rows, t.cols, t.padded_cols, k,
