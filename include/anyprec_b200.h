@@ -131,6 +131,12 @@ void* apb_gemv_plan_create(int n_problems, const uint8_t* const* planes, const i
 int apb_gemv_plan_launch(void* plan, const uint16_t* const* x, void* const* y, void* stream);
 void apb_gemv_plan_destroy(void* plan);
 
+/* engine.py:312-341 small-batch GEMM (SURVEY 8(b) name): apb_gemv over m
+ * activation rows X [m][ldx] -> Y [m][ldy]. */
+int apb_gemm_small(const uint8_t* planes, int n_max, int64_t rows, int64_t cols, int64_t padded_cols, int k,
+                   const uint16_t* lut, int m, const uint16_t* X, int64_t ldx, void* Y, int y_dtype, int64_t ldy,
+                   void* stream);
+
 /* engine.py:357-362 dequantize, from the top-k planes: w [rows][ldw] of
  * w_dtype (fp16 is exact: the values ARE fp16 table entries). */
 int apb_dequant(const uint8_t* planes, int n_max, int64_t rows, int64_t cols,
@@ -230,6 +236,13 @@ int apb_gemv_grouped_peers(int n_problems, const uint8_t* const* planes, const i
                            const uint16_t* const* x, int m_x, const int64_t* ldx, int x_split, void* const* y,
                            int y_dtype, const int64_t* ldy, int n_peers, void* const* y_peers,
                            uint32_t* const* peer_flags, int flags, void* stream);
+/* SURVEY 8(b) name of the single-layer form: this rank's row slab
+ * [row_offset, row_offset + rows) of a [m_x][ldy] output written into every
+ * rank's output y_ranks[r] (as mapped here) + the arrival counters flag_ranks[r]. */
+int apb_gemv_allgather(const uint8_t* planes, int n_max, int64_t rows, int64_t cols, int64_t padded_cols, int k,
+                       const uint16_t* lut, const uint16_t* x, int m_x, int64_t ldx, int rank, int world,
+                       void* const* y_ranks, int64_t row_offset, int y_dtype, int64_t ldy,
+                       uint32_t* const* flag_ranks, int flags, void* stream);
 int apb_peer_wait(const uint32_t* arrivals, uint32_t* expected, uint32_t per_step, int* status,
                   long long spin_limit, void* stream);
 int apb_peer_alloc(int64_t bytes, void** ptr, void* handle);

@@ -1272,3 +1272,37 @@ extern "C" int apb_gemv(const uint8_t* planes, int n_max, int64_t rows, int64_t 
     return apb_gemv_grouped(1, &planes, &n_max, &rows, &cols, &padded_cols, k, &lut, &x, m_x, &ldx,
                             x_split, &y, y_dtype, &ldy, flags, stream);
 }
+
+// SURVEY 8(b) names.  Small-batch GEMM (engine.py:312-341, M <= dense
+// threshold): the quantized kernel over M activation rows.
+extern "C" int apb_gemm_small(const uint8_t* planes, int n_max, int64_t rows, int64_t cols, int64_t padded_cols,
+                              int k, const uint16_t* lut, int m, const uint16_t* X, int64_t ldx, void* Y,
+                              int y_dtype, int64_t ldy, void* stream) {
+    return apb_gemv(planes, n_max, rows, cols, padded_cols, k, lut, X, m, ldx, 0, Y, y_dtype, ldy, 0, stream);
+}
+
+// Row-sharded GEMV + all-gather of one layer: this rank's slab
+// [row_offset, row_offset + rows) of a [m][ldy] output, written into every
+// rank's output (y_ranks[r]: rank r's output as mapped here) with the arrival
+// counters flag_ranks[r]; complete it with apb_peer_wait on flag_ranks[rank].
+extern "C" int apb_gemv_allgather(const uint8_t* planes, int n_max, int64_t rows, int64_t cols,
+                                  int64_t padded_cols, int k, const uint16_t* lut, const uint16_t* x, int m_x,
+                                  int64_t ldx, int rank, int world, void* const* y_ranks, int64_t row_offset,
+                                  int y_dtype, int64_t ldy, uint32_t* const* flag_ranks, int flags, void* stream) {
+    if (world < 1 || world > 8 || rank < 0 || rank >= world || !y_ranks || !flag_ranks || row_offset < 0)
+        return APB_ERR_PARAM;
+    const int64_t esz = y_dtype == APB_DTYPE_F16 ? 2 : 4;
+    void* own = static_cast<uint8_t*>(y_ranks[rank]) + row_offset * esz;
+    void* peers[8];
+    uint32_t* fl[9];
+    int np = 0;
+    for (int r = 0; r < world; ++r)
+        if (r != rank) {
+            if (!y_ranks[r]) return APB_ERR_PARAM;
+            peers[np] = static_cast<uint8_t*>(y_ranks[r]) + row_offset * esz;
+            fl[np++] = flag_ranks[r];
+        }
+    fl[np] = flag_ranks[rank];
+    return apb_gemv_grouped_peers(1, &planes, &n_max, &rows, &cols, &padded_cols, k, &lut, &x, m_x, &ldx, 0, &own,
+                                  y_dtype, &ldy, np, peers, fl, flags, stream);
+}

@@ -138,3 +138,52 @@ def test_fused_allgather_two_processes_ipc():
         assert p.exitcode == 0
     res = sorted(q.get(timeout=10) for _ in range(2))
     assert all(ok for _, ok in res), res
+
+
+def test_survey_named_entry_points_allgather_and_gemm_small():
+    """apb_gemv_allgather (2 simulated ranks, each rank's slab into both outputs,
+    then apb_peer_wait) and apb_gemm_small give the plain kernel's numbers."""
+    import ctypes
+
+    import torch
+
+    from paper_2402_10517_b200 import _device as dev
+    from paper_2402_10517_b200 import dist, engine, plan
+    from paper_2402_10517_b200._lib import APB_DTYPE_F32, check, load, ptr_array
+
+    lib, P, st = load(), dev.ptr, dev.stream_ptr()
+    L = _layer(8, 900, 2048)
+    full = engine.prepare(L)
+    x = torch.randn(1, 2048, device="cuda").half()
+    ref = plan.GemvPlan([full], 5, grouped=True)
+    ref.x[0].copy_(x)
+    ref.run()
+    # gemm_small: M = 3 rows through the SURVEY-named entry point
+    X = torch.randn(3, 2048, device="cuda").half()
+    Y = torch.empty(3, 900, device="cuda")
+    t = full.tensor
+    check(lib.apb_gemm_small(P(t.planes), t.n_max, t.rows, t.cols, t.padded_cols, 5, P(full.tables16[5]), 3, P(X),
+                             2048, P(Y), APB_DTYPE_F32, 900, st), "apb_gemm_small")
+    Yr = engine.gemm(full, X, engine.GemvConfig(bit_width=5, activations_fp16=True))
+    assert torch.equal(Y, Yr)
+    # allgather, world 2 on one GPU
+    outs = [torch.zeros(1, 900, device="cuda") for _ in range(2)]
+    ctrl = [torch.zeros(4, dtype=torch.int32, device="cuda") for _ in range(2)]  # arrivals, expected, status
+    yr = ptr_array([P(o) for o in outs])
+    fr = ptr_array([P(c) for c in ctrl])
+    PP = lambda a: ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))  # noqa: E731
+    for r in range(2):
+        shard = engine.prepare(dist.shard_layer(L, 2, r))
+        r0, _ = dist.shard_bounds(900, 2, r)
+        s_ = shard.tensor
+        check(lib.apb_gemv_allgather(P(s_.planes), s_.n_max, s_.rows, s_.cols, s_.padded_cols, 5,
+                                     P(shard.tables16[5]), P(x), 1, 2048, r, 2, PP(yr), r0, APB_DTYPE_F32, 900,
+                                     PP(fr), 0, st), "apb_gemv_allgather")
+    for r in range(2):
+        c = ctrl[r]
+        check(lib.apb_peer_wait(P(c), P(c) + 4, 900, P(c) + 8, 1 << 20, st), "apb_peer_wait")
+    torch.cuda.synchronize()
+    for r in range(2):
+        assert int(ctrl[r][2]) == 0
+        assert torch.allclose(outs[r], ref.y[0], rtol=1e-5, atol=1e-5)
+    assert torch.equal(outs[0], outs[1])
