@@ -216,8 +216,14 @@ def measured_traffic():
         k = int(tr["launches"][0]["kernel"].split("<")[1].split(">")[0].split(",")[0])
         alg = [sum(alg_bytes(SHAPES[j][1], SHAPES[j][2], k) for j in grp) for grp in GROUPS]
         ratio = sum(dram) / sum(alg)
-        return round(ratio * step_bytes()), {"dram_over_algorithmic": round(ratio, 4), "k": k,
-                                             "source": tr["source"]}
+        launches = len(BITS) * len(GROUPS)
+        # per launch, like `achieved`: the average GEMV launch of a step
+        return round(ratio * step_bytes() / launches), {
+            "dram_over_algorithmic": round(ratio, 4), "k": k, "source": tr["source"],
+            "algorithmic_bytes_per_launch": round(step_bytes() / launches),
+            "dram_bytes_per_step": round(ratio * step_bytes()),
+            "captured_launches": [{"group": "+".join(SHAPES[j][0] for j in grp), "dram_bytes": d, "alg_bytes": a}
+                                  for grp, d, a in zip(GROUPS, dram, alg)]}
     except Exception:
         return None, None
 
@@ -337,9 +343,10 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": round(value, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(value / peak, 4), "peak_kind": peak_kind, "traffic": traffic,
                      "traffic_detail": traffic_detail,
-                     "note": "achieved = algorithmic bytes / CUDA-event time of the timed region "
-                             "(every launch in it is the GEMV kernel); traffic = DRAM bytes per step "
-                             "estimated from the committed ncu capture"},
+                     "note": "achieved = algorithmic bytes per GEMV launch / average launch time (CUDA "
+                             "events over the timed region, every launch in it is the GEMV kernel: "
+                             "= step bytes / step time); traffic = DRAM bytes per average launch from "
+                             "the committed ncu --set full capture (dram_over_algorithmic x algorithmic)"},
         "clocks": clocks,
     }
     if args.profile:
