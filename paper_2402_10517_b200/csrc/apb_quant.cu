@@ -31,7 +31,7 @@
 namespace {
 
 constexpr double kTiny = 4.9406564584124654e-324;  // clustering.py:86, smallest subnormal
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLevelBits = 8;                   // quantizer.py:28 MAX_BITS
 constexpr int kMaxIntervals = 1 << kMaxLevelBits;
