@@ -170,6 +170,11 @@ int apb_rope_cache(const uint16_t* q, const uint16_t* k, const uint16_t* v, cons
                    uint16_t* q_out, uint16_t* k_cache, uint16_t* v_cache, int heads, int head_dim,
                    int64_t cache_head_stride, void* stream);
 int apb_silu_mul(const uint16_t* gate, const uint16_t* up, uint16_t* out, int64_t n, void* stream);
+/* decode-step ends: resid = float(embed[*token]) and out = fp16(rmsnorm(resid) * w);
+ * argmax of an fp16 vector (first index on ties) into *out. */
+int apb_embed_rms(const uint16_t* embed, const int64_t* token, int64_t n, float* resid, const uint16_t* w,
+                  uint16_t* out, float eps, void* stream);
+int apb_argmax_f16(const uint16_t* x, int64_t n, int64_t* out, void* stream);
 
 /* Single-query decode attention with RoPE and KV-cache append fused in
  * (head_dim 128).  q, k, v: this token's projections (heads x head_dim fp16);

@@ -397,3 +397,82 @@ extern "C" int apb_attention_decode(const uint16_t* q, const uint16_t* k, const 
                            (__half*)v_cache, cache_head_stride, pos, scale_log2, ws, tickets, (__half*)out,
                            (const __half*)next_k_cache, (const __half*)next_v_cache);
 }
+
+// ---- decode-step ends: embedding row -> residual + first RMSNorm; argmax ----
+namespace {
+
+__global__ void __launch_bounds__(1024) embed_rms_kernel(const __half* __restrict__ embed,
+                                                         const int64_t* __restrict__ token, int n,
+                                                         float* __restrict__ resid, const __half* __restrict__ w,
+                                                         __half* __restrict__ out, float eps) {
+    __shared__ float sh[32];
+    __shared__ float scale;
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const __half* row = embed + token[0] * (int64_t)n;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const float r = __half2float(row[i]);
+        resid[i] = r;
+        ss += r * r;
+    }
+    ss = block_sum(ss, sh);
+    if (threadIdx.x == 0) scale = rsqrtf(ss / n + eps);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        out[i] = __float2half(__half2float(row[i]) * scale * __half2float(w[i]));
+}
+
+// index of the largest value (first one on ties; NaN never wins)
+__global__ void __launch_bounds__(1024) argmax_kernel(const __half* __restrict__ x, int n, int64_t* __restrict__ out) {
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    float bv = -INFINITY;
+    int bi = INT32_MAX;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const float v = __half2float(x[i]);
+        if (v > bv || (v == bv && i < bi)) {
+            bv = v;
+            bi = i;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const float v = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int i = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (v > bv || (v == bv && i < bi)) {
+            bv = v;
+            bi = i;
+        }
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sv[w] = bv;
+        si[w] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int j = 1; j < (int)(blockDim.x >> 5); ++j)
+            if (sv[j] > bv || (sv[j] == bv && si[j] < bi)) {
+                bv = sv[j];
+                bi = si[j];
+            }
+        out[0] = bi == INT32_MAX ? 0 : bi;
+    }
+}
+
+}  // namespace
+
+extern "C" int apb_embed_rms(const uint16_t* embed, const int64_t* token, int64_t n, float* resid,
+                             const uint16_t* w, uint16_t* out, float eps, void* stream) {
+    if (!embed || !token || !resid || !w || !out || n <= 0 || n > INT32_MAX) return APB_ERR_PARAM;
+    return launch_pdl(embed_rms_kernel, (cudaStream_t)stream, (const __half*)embed, token, (int)n, resid,
+                      (const __half*)w, (__half*)out, eps);
+}
+
+extern "C" int apb_argmax_f16(const uint16_t* x, int64_t n, int64_t* out, void* stream) {
+    if (!x || !out || n <= 0 || n > INT32_MAX) return APB_ERR_PARAM;
+    return launch_pdl(argmax_kernel, (cudaStream_t)stream, (const __half*)x, (int)n, out);
+}

@@ -134,10 +134,10 @@ class DecodeModel:
         cfg, ctx = self.cfg, self.context
         nh, hd, H = cfg.heads, cfg.head_dim, cfg.hidden
         P = dev.ptr
-        self.resid.copy_(self.embed[self.token].view(H).float())
         blocks = self._plans_for(k)
-        check(lib.apb_rms_residual(P(self.resid), None, P(self.norm_w), P(blocks[0][0].x[0]), H, 1e-5, st),
-              "apb_rms_residual")
+        # embedding row -> fp32 residual and the first block's normalised input, one kernel
+        check(lib.apb_embed_rms(P(self.embed), P(self.token), H, P(self.resid), P(self.norm_w),
+                                P(blocks[0][0].x[0]), 1e-5, st), "apb_embed_rms")
         for li, (qkv, o, gu, dn) in enumerate(blocks):
             qkv.run()
             check(lib.apb_attention_decode(P(qkv.y[0]), P(qkv.y[1]), P(qkv.y[2]), P(self.cos), P(self.sin),
@@ -151,7 +151,7 @@ class DecodeModel:
         check(lib.apb_rms_residual(P(self.resid), None, P(self.norm_w), P(self.hbuf), H, 1e-5, st),
               "apb_rms_residual")
         logits = self.hbuf @ self.lm_head.t()
-        self.next_token.copy_(torch.argmax(logits, dim=-1))
+        check(lib.apb_argmax_f16(P(logits), cfg.vocab, P(self.next_token), st), "apb_argmax_f16")
 
     def _next_kv(self, li):
         """The next block's cache for the attention kernel's L2 prefetch (none after the last)."""

@@ -154,3 +154,33 @@ def test_rms_residual_and_silu_vs_fp32(n):
     torch.cuda.synchronize()
     want = torch.nn.functional.silu(gate.float()) * up.float()
     assert float((out.float() - want).abs().max()) < 1e-2
+
+
+def test_embed_rms_and_argmax():
+    import torch
+
+    from paper_2402_10517_b200 import _device as dev
+    from paper_2402_10517_b200._lib import check, load
+
+    lib, P, st = load(), dev.ptr, dev.stream_ptr()
+    g = torch.Generator(device="cuda").manual_seed(1)
+    emb = torch.randn(100, 4096, device="cuda", generator=g).half()
+    w = (torch.rand(4096, device="cuda", generator=g) + 0.5).half()
+    tok = torch.tensor([37], device="cuda")
+    resid = torch.empty(4096, device="cuda")
+    out = torch.empty(4096, device="cuda", dtype=torch.float16)
+    check(lib.apb_embed_rms(P(emb), P(tok), 4096, P(resid), P(w), P(out), 1e-5, st), "apb_embed_rms")
+    torch.cuda.synchronize()
+    r = emb[37].float()
+    assert torch.equal(resid, r)
+    want = r * torch.rsqrt(r.pow(2).mean() + 1e-5) * w.float()
+    assert float((out.float() - want).abs().max()) < 4e-3
+    for n in (1, 1000, 32000):
+        x = torch.randn(n, device="cuda", generator=g).half()
+        x[n // 2] = 60000.0
+        if n > 10:
+            x[n // 3] = 60000.0  # tie: the first index wins
+        o = torch.empty(1, dtype=torch.int64, device="cuda")
+        check(lib.apb_argmax_f16(P(x), n, P(o), st), "apb_argmax_f16")
+        torch.cuda.synchronize()
+        assert int(o) == (n // 3 if n > 10 else 0), (n, int(o))
