@@ -341,7 +341,8 @@ def run_ours(args):
                    "l2": f"inputs > L2: weights rotated over {N_COPIES} copies (4 x 203 MB) per launch"},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": round(value, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(value / peak, 4), "peak_kind": peak_kind, "traffic": traffic,
+                     "frac": round(value / peak, 4), "peak_kind": peak_kind,
+                     "frac_of_nominal_8000": round(value / 8000.0, 4), "traffic": traffic,
                      "traffic_detail": traffic_detail,
                      "note": "achieved = algorithmic bytes per GEMV launch / average launch time (CUDA "
                              "events over the timed region, every launch in it is the GEMV kernel: "
