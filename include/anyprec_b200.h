@@ -61,6 +61,11 @@ enum { APB_FLAG_PDL = 1 };
  * TMA kernel only (k 3..8, m_x <= 8, <= 16 problems); else APB_ERR_PARAM. */
 enum { APB_FLAG_GLU = 2 };
 
+/* Host-path plumbing: async copy on a stream (kind 0 H2D, 1 D2H, 2 D2D) and a
+ * stream synchronisation (for bindings without their own CUDA runtime). */
+int apb_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void* stream);
+int apb_stream_sync(void* stream);
+
 /* Library version (major*10000 + minor*100 + patch) and status strings. */
 int apb_version(void);
 const char* apb_status_string(int status);

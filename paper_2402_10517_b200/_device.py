@@ -13,16 +13,23 @@ def torch():
     return _t
 
 
+_CUDA_OK = False
+
+
 def require_cuda():
+    global _CUDA_OK
     t = torch()
-    if not t.cuda.is_available():
-        raise DeviceError("no CUDA device: the B200 kernels have no CPU fallback")
+    if not _CUDA_OK:  # once a device was found it stays there: skip the per-call probe
+        if not t.cuda.is_available():
+            raise DeviceError("no CUDA device: the B200 kernels have no CPU fallback")
+        _CUDA_OK = True
     return t
 
 
 def stream_ptr():
+    """The current torch CUDA stream of the current device (raw handle)."""
     t = require_cuda()
-    return t.cuda.current_stream().cuda_stream
+    return t._C._cuda_getCurrentRawStream(t._C._cuda_getDevice())
 
 
 def is_tensor(a) -> bool:

@@ -70,6 +70,8 @@ SIGNATURES = {
     "apb_silu_mul": ([_P, _P, _P, _I64, _P], _I),
     "apb_embed_rms": ([_P, _P, _I64, _P, _P, _P, ctypes.c_float, _P], _I),
     "apb_argmax_f16": ([_P, _I64, _P, _P], _I),
+    "apb_memcpy_async": ([_P, _P, _I64, _I, _P], _I),
+    "apb_stream_sync": ([_P], _I),
     "apb_gemm_small": ([_P, _I, _I64, _I64, _I64, _I, _P, _I, _P, _I64, _P, _I, _I64, _P], _I),
     "apb_gemv_allgather": (
         [_P, _I, _I64, _I64, _I64, _I, _P, _P, _I, _I64, _I, _I, _PP, _I64, _I, _I64, _PP, _I, _P], _I,

@@ -285,16 +285,24 @@ class _CallPlan:
         self.handle = h or None
         self._xa = (ctypes.c_void_p * 1)()
         self._ya = (ctypes.c_void_p * 1)()
+        self._xap = ctypes.cast(self._xa, ctypes.POINTER(ctypes.c_void_p))
+        self._yap = ctypes.cast(self._ya, ctypes.POINTER(ctypes.c_void_p))
+        # host-path constants (pointers / views / sizes resolved once)
+        self.x_ptr, self.y_ptr = dev.ptr(self.x), dev.ptr(self.y)
+        self.x_pin_ptr, self.y_pin_ptr = dev.ptr(self.x_pin), dev.ptr(self.y_pin)
+        self.x_np, self.y_np = self.x_pin.numpy(), self.y_pin.numpy()
+        self.x_bytes, self.y_bytes = self.x.numel() * 2, self.y.numel() * 4
 
-    def launch(self, xptr=None, yptr=None):
+    def launch(self, xptr=None, yptr=None, stream=None):
         xa = ya = None
         if xptr is not None:
             self._xa[0] = xptr
-            xa = ctypes.cast(self._xa, ctypes.POINTER(ctypes.c_void_p))
+            xa = self._xap
         if yptr is not None:
             self._ya[0] = yptr
-            ya = ctypes.cast(self._ya, ctypes.POINTER(ctypes.c_void_p))
-        check(self._lib.apb_gemv_plan_launch(self.handle, xa, ya, dev.stream_ptr()), "apb_gemv_plan_launch")
+            ya = self._yap
+        check(self._lib.apb_gemv_plan_launch(self.handle, xa, ya, dev.stream_ptr() if stream is None else stream),
+              "apb_gemv_plan_launch")
 
     def __del__(self):
         if getattr(self, "handle", None):
@@ -327,12 +335,13 @@ def _quantized(prep: PreparedLayer, x2, k: int, fp16: bool):
         rows16, m_x, split = _host_rows(x2, m, fp16)
         plan = prep._call_plan(k, m_x, split)
         if plan.handle is not None:
-            plan.x_pin.numpy()[:, :t.cols] = rows16
-            plan.x.copy_(plan.x_pin, non_blocking=True)
-            plan.launch(dev.ptr(plan.x), dev.ptr(plan.y))  # (a device call may have re-pointed the plan)
-            plan.y_pin.copy_(plan.y, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            out = plan.y_pin.numpy().copy()
+            plan.x_np[:, :t.cols] = rows16
+            lib, st = plan._lib, dev.stream_ptr()
+            check(lib.apb_memcpy_async(plan.x_ptr, plan.x_pin_ptr, plan.x_bytes, 0, st), "apb_memcpy_async")
+            plan.launch(plan.x_ptr, plan.y_ptr, st)  # (a device call may have re-pointed the plan)
+            check(lib.apb_memcpy_async(plan.y_pin_ptr, plan.y_ptr, plan.y_bytes, 1, st), "apb_memcpy_async")
+            check(lib.apb_stream_sync(st), "apb_stream_sync")
+            out = plan.y_np.copy()
             return out if not dev.is_tensor(x2) else torch.from_numpy(out)
     xdev, m_x, ldx, split, kind = _stage_x(x2, t.cols, fp16)
     m_out = m_x // 2 if split else m_x
