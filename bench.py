@@ -277,6 +277,16 @@ def run_ours(args):
         torch.cuda.synchronize()
         bad = torch.tensor([max(sp.gather.status() for sp in fused)], device="cuda", dtype=torch.int32)
         dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if not int(bad.item()):  # and the gathered numbers: the first launch vs plain GEMV + NCCL
+            sp, (_, grp, p) = fused[0], plans[0]
+            p.x[0].copy_(sp.x[0])
+            p.run()
+            sp.run()
+            torch.cuda.synchronize()
+            same = all(torch.equal(sp.y[j], gather_rows(p.y[j], SHAPES[li][1]).to(sp.y[j].dtype))
+                       for j, li in enumerate(grp))
+            bad.fill_(0 if same else 1)
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
         if int(bad.item()):
             print("[bench] fused gather self-check failed; using NCCL", file=sys.stderr)
             fused, gather_mode = None, "nccl all_gather_into_tensor after each GEMV (fused self-check failed)"
