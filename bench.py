@@ -166,21 +166,32 @@ def decode_plans(plan_mod, copies, pdl: bool):
 
 def fused_plans(torch, copies):
     """The decode launch pattern with the all-gather fused into every GEMV
-    (dist.ShardedGemvPlan): one IPC-mapped output block per launch."""
+    (dist.ShardedGemvPlan): one IPC-mapped output block per launch.  Every rank
+    makes the same collective calls; None (on every rank) unless every rank
+    mapped every peer's blocks."""
+    import torch.distributed as dist
+
     from paper_2402_10517_b200 import dist as pdist
 
-    out, i = [], 0
+    specs, gathers, i = [], [], 0
     for k in BITS:
         for grp in GROUPS:
-            c = copies[i % len(copies)]
             full_rows = [SHAPES[j][1] for j in grp]
             _, nbytes = pdist.output_layout(full_rows, 1, 2)
-            g = pdist.PeerGather(nbytes)
-            sp = pdist.ShardedGemvPlan([c[j] for j in grp], full_rows, k, g, m=1, y_fp16=True,
-                                       shared_x=len(grp) > 1)
-            sp.x[0].normal_()
-            out.append(sp)
+            gathers.append(pdist.PeerGather(nbytes))
+            specs.append((k, grp, copies[i % len(copies)], full_rows))
             i += 1
+    bad = torch.tensor([0 if all(g.ok for g in gathers) else 1], device="cuda", dtype=torch.int32)
+    dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+    if int(bad.item()):
+        for g in gathers:
+            g.close()
+        return None
+    out = []
+    for (k, grp, c, full_rows), g in zip(specs, gathers):
+        sp = pdist.ShardedGemvPlan([c[j] for j in grp], full_rows, k, g, m=1, y_fp16=True, shared_x=len(grp) > 1)
+        sp.x[0].normal_()
+        out.append(sp)
     return out
 
 
@@ -252,11 +263,11 @@ def run_ours(args):
     if world > 1:
         gather_mode = "nccl all_gather_into_tensor after each GEMV"
         if not args.nccl_gather:
-            try:
-                fused = fused_plans(torch, copies)
+            fused = fused_plans(torch, copies)  # collective on every rank; None if any rank lacks P2P / IPC
+            if fused is None:
+                print("[bench] fused gather unavailable (CUDA IPC / P2P); using NCCL", file=sys.stderr)
+            else:
                 gather_mode = "fused: GEMV epilogue stores over NVLink P2P + arrival counters"
-            except Exception as e:  # no P2P / IPC between these GPUs
-                print(f"[bench] fused gather unavailable ({e}); using NCCL", file=sys.stderr)
 
     def step():
         if fused is not None:

@@ -147,9 +147,12 @@ class PeerGather:
     from here.  Control words at ``ctrl_off``: arrivals, expected, status."""
 
     def __init__(self, nbytes: int, group=None):
+        """Collective-safe: every rank takes part in the same handle exchange and
+        barrier whatever fails locally; ``ok`` says whether THIS rank mapped every
+        peer (callers agree on it across ranks before using the block)."""
         import torch.distributed as dist
 
-        from ._lib import check, load
+        from ._lib import load
 
         lib = load()
         self._lib = lib
@@ -157,22 +160,29 @@ class PeerGather:
         self.rank = dist.get_rank(group)
         self.nbytes = nbytes
         self.ctrl_off = nbytes - _CTRL_BYTES
+        self._own, self._opened, self.bases, self.ok = None, [], [], True
         hb = lib.apb_peer_handle_bytes()
         handle = ctypes.create_string_buffer(hb)
         ptr = ctypes.c_void_p()
-        check(lib.apb_peer_alloc(nbytes, ctypes.byref(ptr), handle), "apb_peer_alloc")
-        self._own = ptr.value
+        mine = None
+        if lib.apb_peer_alloc(nbytes, ctypes.byref(ptr), handle) == 0:
+            self._own = ptr.value
+            mine = bytes(handle.raw)
         handles = [None] * self.world
-        dist.all_gather_object(handles, bytes(handle.raw), group=group)
-        self.bases, self._opened = [], []
-        for r, h in enumerate(handles):
-            if r == self.rank:
-                self.bases.append(self._own)
-                continue
-            p = ctypes.c_void_p()
-            check(lib.apb_peer_open(ctypes.create_string_buffer(h, hb), ctypes.byref(p)), "apb_peer_open")
-            self.bases.append(p.value)
-            self._opened.append(p.value)
+        dist.all_gather_object(handles, mine, group=group)
+        if any(h is None for h in handles):
+            self.ok = False
+        else:
+            for r, h in enumerate(handles):
+                if r == self.rank:
+                    self.bases.append(self._own)
+                    continue
+                p = ctypes.c_void_p()
+                if lib.apb_peer_open(ctypes.create_string_buffer(h, hb), ctypes.byref(p)) != 0:
+                    self.ok = False
+                    break
+                self.bases.append(p.value)
+                self._opened.append(p.value)
         dist.barrier(group)
 
     @classmethod
@@ -184,7 +194,7 @@ class PeerGather:
         out = []
         for r in range(world):
             g = cls.__new__(cls)
-            g._lib, g.world, g.rank, g.nbytes = None, world, r, nbytes
+            g._lib, g.world, g.rank, g.nbytes, g.ok = None, world, r, nbytes, True
             g.ctrl_off = nbytes - _CTRL_BYTES
             g.bases = [dev.ptr(b) for b in blocks]
             g._own, g._opened, g._blocks = g.bases[r], [], blocks
@@ -216,8 +226,9 @@ class PeerGather:
             return
         for p in self._opened:
             self._lib.apb_peer_close(p)
-        self._lib.apb_peer_free(self._own)
-        self._opened, self._lib = [], None
+        if self._own:
+            self._lib.apb_peer_free(self._own)
+        self._opened, self._own, self._lib = [], None, None
 
 
 def _wrap_device_bytes(torch, address: int, nbytes: int):
