@@ -49,6 +49,11 @@ def cases():
     w = rng.standard_normal((2, 9000))
     s = rng.random((2, 9000))
     yield "wide_2x9000_3_5", w, s, 3, 5
+    # seed only (n_min == n_max) and a 32-cluster seed (many DP layers)
+    w = rng.standard_normal((6, 500))
+    yield "single_6x500_4_4", w, rng.random((6, 500)), 4, 4
+    w = rng.standard_normal((4, 1200)) * rng.uniform(0.1, 2.0, (4, 1))
+    yield "seed5_4x1200_5_7", w, rng.random((4, 1200)), 5, 7
 
 
 def main():
