@@ -3,6 +3,8 @@
 3..8, activation rows 1..8, fp32 or fp16 activations, single calls and grouped
 launches (separate or shared activations, fp16 / fp32 outputs)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -19,7 +21,7 @@ def _layer(rng, rows, cols, n_min=3, n_max=8):
     return AnyPrecisionLayer(n_min=n_min, n_max=n_max, codes=codes, centroid_tables=tables, shape=(rows, cols))
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("APB_FUZZ_SINGLE", "12"))))
 def test_random_shapes_vs_oracle(seed):
     from paper_2402_10517_b200 import engine
 
@@ -40,7 +42,7 @@ def test_random_shapes_vs_oracle(seed):
     assert ora.rel_err(y, want) < TOL, (rows, cols, k, m, fp16, ora.rel_err(y, want))
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("APB_FUZZ_GROUPED", "8"))))
 def test_random_grouped_launches_vs_oracle(seed):
     import torch
 
