@@ -1133,7 +1133,7 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
         if (ldy[i] < (glu ? rows[i] / 2 : rows[i])) return APB_ERR_SHAPE;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    if (m_x <= 8 && n_problems <= 16) {  // TMA-fed kernel (apb_gemv7.cu)
+    if (m_x <= 16 && n_problems <= 16) {  // TMA-fed kernel (apb_gemv7.cu)
         const int rc = apb7_try_gemv(n_problems, planes, n_max, rows, cols, padded_cols, k, lut, x, m_x, ldx, 0,
                                      x_split, y, y_dtype, ldy, 0, flags, stream, 0, nullptr, nullptr, nullptr);
         if (rc != -1) return rc;
@@ -1169,7 +1169,7 @@ extern "C" void* apb_gemv_plan_create(int n_problems, const uint8_t* const* plan
                                       const int64_t* ldy, int flags) {
     if (n_problems < 1 || n_problems > 16 || k < 3 || k > 8) return nullptr;
     if (y_dtype != APB_DTYPE_F32 && y_dtype != APB_DTYPE_F16) return nullptr;
-    if (m_x < 1 || m_x > 8 || (x_split && (m_x & 1))) return nullptr;
+    if (m_x < 1 || m_x > 16 || (x_split && (m_x & 1))) return nullptr;
     const bool glu = (flags & APB_FLAG_GLU) != 0;
     for (int i = 0; i < n_problems; ++i) {
         if (rows[i] <= 0 || cols[i] <= 0 || (glu && (rows[i] & 1))) return nullptr;
@@ -1200,7 +1200,7 @@ extern "C" int apb_gemv_grouped_peers(int n_problems, const uint8_t* const* plan
     if (n_problems < 1) return APB_ERR_SHAPE;
     if (k < 3 || k > 8) return APB_ERR_PARAM;  // the TMA kernel's range
     if (y_dtype != APB_DTYPE_F32 && y_dtype != APB_DTYPE_F16) return APB_ERR_PARAM;
-    if (m_x < 1 || m_x > 8 || n_problems > 16 || (x_split && (m_x & 1))) return APB_ERR_SHAPE;
+    if (m_x < 1 || m_x > 16 || n_problems > 16 || (x_split && (m_x & 1))) return APB_ERR_SHAPE;
     if (n_peers < 0 || n_peers > 7 || (n_peers > 0 && !y_peers) || !peer_flags) return APB_ERR_PARAM;
     for (int j = 0; j <= n_peers; ++j)
         if (!peer_flags[j] || ((uintptr_t)peer_flags[j] & 3)) return APB_ERR_PARAM;
@@ -1232,7 +1232,7 @@ extern "C" int apb_gemv_grouped_norm(int n_problems, const uint8_t* const* plane
     if (!norm || norm->mode < 0 || norm->mode > 2) return APB_ERR_PARAM;
     if (n_problems < 1 || n_problems > 16) return APB_ERR_SHAPE;
     if (k < 3 || k > 8 || (y_dtype != APB_DTYPE_F16 && y_dtype != APB_DTYPE_F32)) return APB_ERR_PARAM;
-    if (m_x < 1 || m_x > 8) return APB_ERR_SHAPE;
+    if (m_x < 1 || m_x > 16) return APB_ERR_SHAPE;
     const bool glu = (flags & APB_FLAG_GLU) != 0;
     if (norm->mode == 1) {  // producer: one batch row, one problem, fp16 normalised output
         if (m_x != 1 || n_problems != 1 || glu || y_dtype != APB_DTYPE_F16) return APB_ERR_PARAM;

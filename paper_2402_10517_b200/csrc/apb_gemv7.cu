@@ -120,7 +120,7 @@ struct Geo {
     // up to 8 batch rows in the MMA N dimension); its table is
     // [slot (64 KB stride)][entry][row-half 2][lane 32] u32.  Otherwise the
     // row-copy mapping: [entry][slot 2][lane 32] u32.
-    static constexpr bool kMapN = NB == 4;
+    static constexpr bool kMapN = NB >= 4;  // NB == 8: 16 batch rows, two MMAs per A fragment
     static constexpr int kTableBytes = kMapN ? 65536 + kEntries * 256 : kEntries * 256;
     static constexpr int kLutHalves = 1 << K;
     static constexpr int kLutBox = kLutHalves < 64 ? kLutHalves : 64;  // halves per box row
@@ -133,7 +133,7 @@ struct Geo {
 #else
     // compute warps, groups of 4 (measured best per k; 8 for 4 batch pairs: registers;
     // 8 when two CTAs share an SM)
-    static constexpr int kWC = NB == 4 ? 12 : (CPS == 2 ? 8 : (K == 8 ? 12 : 16));
+    static constexpr int kWC = NB == 8 ? 8 : (NB == 4 ? 12 : (CPS == 2 ? 8 : (K == 8 ? 12 : 16)));
 #endif
     static constexpr int kNG = kWC / 4;
     static constexpr int kThreads = (kWC + 2) * 32;
@@ -724,6 +724,8 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
         const int c = su + 4 * (q >> 1), hf = q & 1;
         const uint32_t po0 = g * 128 + ((c ^ g) << 4) + hf * 8, po1 = po0 + 8 * 128;  // rows g, g+8 (same swizzle)
         const int gm = g < L.m_x ? g : L.m_x - 1;
+        const int gm2 = 8 + g < L.m_x ? 8 + g : L.m_x - 1;  // NB == 8: batch rows 8..15 (second MMA)
+        constexpr int kBR = 2 * NB;                          // batch rows of the partials
         const int xcol0 = 8 * (4 * c + 2 * hf);  // column of word wi=0, p=0 (+ tile*1024 + 256p + 8wi)
         int pi = problem_of(L, first), pend = problem_end(L, pi);
         int gs = grp, item_gs = 0, slot = grp, ph = 0;
@@ -737,12 +739,16 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
             const Prob7& P = L.prob[pi];
             const int nt = P.n_tiles;
             const uint16_t* const xrow = P.x + (int64_t)gm * P.ldx + xcol0;
+            const uint16_t* const xrow2 = P.x + (int64_t)gm2 * P.ldx + xcol0;
             const int xcols = (int)P.cols - xcol0;
             const int full_tiles = (int)(P.cols / kTileWeights);
             const uint32_t off0 = ((uint32_t)(jl & 1) << 16) | ((uint32_t)lane * 4u), off1 = off0 + 128u;
-            float acc[2][4];
+            float acc[2][4], acc2[2][4];
 #pragma unroll
-            for (int c2 = 0; c2 < 2; ++c2) acc[c2][0] = acc[c2][1] = acc[c2][2] = acc[c2][3] = 0.f;
+            for (int c2 = 0; c2 < 2; ++c2) {
+                acc[c2][0] = acc[c2][1] = acc[c2][2] = acc[c2][3] = 0.f;
+                acc2[c2][0] = acc2[c2][1] = acc2[c2][2] = acc2[c2][3] = 0.f;
+            }
             mbar_sleep(b_tready + 8 * (jl & 1), (jl >> 1) & 1);
             if (jl == 0) {
                 asm volatile("griddepcontrol.wait;" ::: "memory");  // x from the previous kernel
@@ -764,19 +770,21 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
 #pragma unroll
                     for (int wi = 0; wi < 2; ++wi) {
                         const int cbase = tile * kTileWeights + 8 * wi;  // + 256p, relative to xcol0
-                        uint4 xq[4];
+                        uint4 xq[4], xq2[4];
 #pragma unroll
                         for (int p = 0; p < 4; ++p) {
                             const int c0 = cbase + 256 * p;
-                            const uint16_t* src = xrow + c0;
-                            if (kTail && c0 >= xcols) src = g_zero_x;  // never read past ldx
-                            xq[p] = __ldg(reinterpret_cast<const uint4*>(src));
+                            const bool past = kTail && c0 >= xcols;  // never read past ldx
+                            xq[p] = __ldg(reinterpret_cast<const uint4*>(past ? g_zero_x : xrow + c0));
+                            if constexpr (NB == 8) xq2[p] = __ldg(reinterpret_cast<const uint4*>(past ? g_zero_x : xrow2 + c0));
                             if constexpr (kTail) {
-                                uint32_t w[4] = {xq[p].x, xq[p].y, xq[p].z, xq[p].w};
+                                uint32_t mk[4];
 #pragma unroll
                                 for (int h = 0; h < 4; ++h)
-                                    w[h] &= (c0 + 2 * h < xcols ? 0x0000FFFFu : 0u) | (c0 + 2 * h + 1 < xcols ? 0xFFFF0000u : 0u);
-                                xq[p] = make_uint4(w[0], w[1], w[2], w[3]);
+                                    mk[h] = (c0 + 2 * h < xcols ? 0x0000FFFFu : 0u) | (c0 + 2 * h + 1 < xcols ? 0xFFFF0000u : 0u);
+                                xq[p] = make_uint4(xq[p].x & mk[0], xq[p].y & mk[1], xq[p].z & mk[2], xq[p].w & mk[3]);
+                                if constexpr (NB == 8)
+                                    xq2[p] = make_uint4(xq2[p].x & mk[0], xq2[p].y & mk[1], xq2[p].z & mk[2], xq2[p].w & mk[3]);
                             }
                         }
                         uint32_t Qa[K], Qb[K];
@@ -799,9 +807,14 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
 #pragma unroll
                         for (int p = 0; p < 4; ++p)
 #pragma unroll
-                            for (int jj = 0; jj < 2; ++jj)
+                            for (int jj = 0; jj < 2; ++jj) {
                                 mma16816(acc[p & 1], a0[p * 4 + 2 * jj], a1[p * 4 + 2 * jj], a0[p * 4 + 2 * jj + 1],
                                          a1[p * 4 + 2 * jj + 1], u4w(xq[p], 2 * jj), u4w(xq[p], 2 * jj + 1));
+                                if constexpr (NB == 8)  // the same A fragment against batch rows 8..15
+                                    mma16816(acc2[p & 1], a0[p * 4 + 2 * jj], a1[p * 4 + 2 * jj],
+                                             a0[p * 4 + 2 * jj + 1], a1[p * 4 + 2 * jj + 1], u4w(xq2[p], 2 * jj),
+                                             u4w(xq2[p], 2 * jj + 1));
+                            }
                     }
                 };
                 if (tile < full_tiles)
@@ -811,11 +824,17 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
             }
             item_gs += nt;
             // D[g][2q..2q+1] / D[g+8][2q..2q+1]: rows g, g+8 of batch rows 2q, 2q+1
-            float* r = red + (jl & 1) * (WC * 8 * kRows) + warp * 8 * kRows;
+            float* r = red + (jl & 1) * (WC * kBR * kRows) + warp * kBR * kRows;
             r[(2 * q) * kRows + g] = acc[0][0] + acc[1][0];
             r[(2 * q + 1) * kRows + g] = acc[0][1] + acc[1][1];
             r[(2 * q) * kRows + g + 8] = acc[0][2] + acc[1][2];
             r[(2 * q + 1) * kRows + g + 8] = acc[0][3] + acc[1][3];
+            if constexpr (NB == 8) {  // batch rows 8 + 2q, 8 + 2q + 1
+                r[(8 + 2 * q) * kRows + g] = acc2[0][0] + acc2[1][0];
+                r[(8 + 2 * q + 1) * kRows + g] = acc2[0][1] + acc2[1][1];
+                r[(8 + 2 * q) * kRows + g + 8] = acc2[0][2] + acc2[1][2];
+                r[(8 + 2 * q + 1) * kRows + g + 8] = acc2[0][3] + acc2[1][3];
+            }
             mbar_arrive(b_idone + 8 * (jl & 1));
         }
         return;
@@ -1174,7 +1193,7 @@ int apb7_build(Launch7& L, int& nb, int n, const uint8_t* const* planes, const i
                const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split, void* const* y,
                int y_dtype, const int64_t* ldy, int64_t y_off, int flags, int n_peers, void* const* y_peers,
                uint32_t* const* peer_flags, const apb_norm_epilogue* norm) {
-    if (k < 3 || k > 8 || m_x > 8 || n > kMaxProb || n_peers > kMaxPeers - 1) return -1;
+    if (k < 3 || k > 8 || m_x > 16 || n > kMaxProb || n_peers > kMaxPeers - 1) return -1;
     for (int i = 0; i < n; ++i)
         if (padded[i] > kMaxCols) return -1;
     std::memset(&L, 0, sizeof(L));
@@ -1240,19 +1259,20 @@ int apb7_build(Launch7& L, int& nb, int n, const uint8_t* const* planes, const i
 #ifndef APB7_NB2_MAX
 #define APB7_NB2_MAX 2
 #endif
-    nb = m_x <= 2 ? 1 : (m_x <= APB7_NB2_MAX ? 2 : 4);
+    nb = m_x <= 2 ? 1 : (m_x <= APB7_NB2_MAX ? 2 : (m_x <= 8 ? 4 : 8));
     if (nb > 1) L.xs_bytes = 0;
     return 0;
 }
 
 int apb7_dispatch(Launch7& L, int k, int nb, int flags, cudaStream_t s) {
     const bool epi = L.glu || L.norm_mode || L.n_peers >= 0;
-    switch (k * 8 + nb) {
+    switch (k * 16 + nb) {
 #define APB7_L(K, NB, CPS) (epi ? launch<K, NB, CPS, true>(L, flags, s) : launch<K, NB, CPS, false>(L, flags, s))
 #define APB7_CASE(K)                                                           \
-    case K * 8 + 1: return choose_cps<K, 1>(L) == 2 ? APB7_L(K, 1, 2) : APB7_L(K, 1, 1); \
-    case K * 8 + 2: return APB7_L(K, 2, 1);                                    \
-    case K * 8 + 4: return APB7_L(K, 4, 1);
+    case K * 16 + 1: return choose_cps<K, 1>(L) == 2 ? APB7_L(K, 1, 2) : APB7_L(K, 1, 1); \
+    case K * 16 + 2: return APB7_L(K, 2, 1);                                    \
+    case K * 16 + 4: return APB7_L(K, 4, 1);                                    \
+    case K * 16 + 8: return APB7_L(K, 8, 1);
         APB7_CASE(3)
         APB7_CASE(4)
         APB7_CASE(5)
