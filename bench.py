@@ -518,12 +518,13 @@ def _chain_us(torch, plan, preps_copies, k, m, reps=10):
 def small_batch_detail(torch, plan, copies):
     """BASELINE config C3: any-precision GEMM at batch M = 1, 2, 4, 8 on the
     Llama-2-7B MLP shapes (gate/up 11008x4096, down 4096x11008) at k = 3, 4, 8
-    (fp16 activations, each decoded weight reused across the batch)."""
+    (fp16 activations, each decoded weight reused across the batch); plus M = 16,
+    the top of the reference's quantized range (dense_threshold)."""
     out = {}
     for li, name in ((4, "gate_11008x4096"), (6, "down_4096x11008")):
         r, c = SHAPES[li][1], SHAPES[li][2]
         for k in (3, 4, 8):
-            for m in (1, 2, 4, 8):
+            for m in (1, 2, 4, 8, 16):
                 us = _chain_us(torch, plan, [cp[li] for cp in copies], k, m)
                 out.setdefault(name, {}).setdefault(f"k{k}", {})[f"M{m}"] = {
                     "us": round(us, 2), "GBps": round(alg_bytes(r, c, k, m) / (us * 1e-6) / 1e9, 1)}
@@ -533,8 +534,9 @@ def small_batch_detail(torch, plan, copies):
 def shard70b_detail(torch, plan):
     """BASELINE config C4 on one GPU: the per-rank GEMV of the Llama-2-70B layer
     shapes row-sharded over P = 1, 2, 4, 8 ranks (each rank owns a contiguous
-    R/P-row slab; k = 3, 4, 8).  The NCCL all-gather of the y slices that follows
-    on a multi-GPU box is not part of this single-GPU number."""
+    R/P-row slab; k = 3, 4, 8).  The all-gather of the y slices that follows on a
+    multi-GPU box (fused into the GEMV epilogue there) is not part of this
+    single-GPU number."""
     from paper_2402_10517_b200 import AnyPrecisionLayer, engine
 
     shapes = [("8192x8192", 8192, 8192), ("28672x8192", 28672, 8192), ("8192x28672", 8192, 28672)]
