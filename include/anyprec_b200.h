@@ -292,6 +292,17 @@ int apb_quant_continue(const double* weights, const double* sens, const int64_t*
                        const uint16_t* table_k0, int rows, int n, int k0, int new_n_max, uint8_t* codes,
                        uint16_t* tables, double* sse, int* bad, void* workspace, int64_t workspace_bytes,
                        void* stream);
+/* cluster_rows / quantize_seed / kmeans_1d_weighted (clustering.py:204-227,
+ * quantizer.py:122-157, 281-307) for any cluster count 1 <= k <= 4096: per
+ * row the exact weighted k-means bounds over the sorted order ([rows][k+1],
+ * trailing empty intervals of low-distinct rows end at n), float64 centroids
+ * ([rows][k], an empty interval copies the previous column) and, if codes is
+ * not NULL, each element's interval index in original order ([rows][n]).
+ * sens must be coerced by the caller; order is the stable argsort. */
+int64_t apb_quant_cluster_workspace(int rows, int n, int k);
+int apb_quant_cluster(const double* weights, const double* sens, const int64_t* order, int rows, int n, int k,
+                      int* bounds, double* means, int* codes, void* workspace, int64_t workspace_bytes,
+                      void* stream);
 int apb_quant_sse_levels(const double* weights, const double* sens, const uint8_t* codes, int shift,
                          const uint16_t* table_k, int k, int rows, int n, double* sse, void* stream);
 

@@ -140,6 +140,17 @@ __device__ double reduceat_sum(const F& f, int64_t a, int64_t n) {
     return f(a) + pairwise_sum(f, a + 1, n - 1);
 }
 
+// Weighted mean of sorted positions [a, a + len) (clustering.py:60-83): the
+// reduceat sums of w and w*v; zero total weight -> the plain mean; empty -> NaN.
+__device__ double interval_mean(const double* sv, const double* sw, int a, int len) {
+    if (len <= 0) return NAN;
+    const double sum_w = reduceat_sum([&](int64_t i) { return sw[i]; }, a, len);
+    const double sum_wv = reduceat_sum([&](int64_t i) { return sw[i] * sv[i]; }, a, len);
+    if (sum_w > 0.0) return sum_wv / sum_w;
+    const double sum_v = reduceat_sum([&](int64_t i) { return sv[i]; }, a, len);
+    return sum_v / (double)len;
+}
+
 // (value, index) argmin with first-index tie break, as np.minimum.reduceat
 // followed by the first position equal to the minimum.
 __device__ __forceinline__ void argmin_merge(double& v, int& i, double v2, int i2) {
@@ -361,21 +372,7 @@ __global__ void __launch_bounds__(kThreads) level_kernel(int rows, Ws W, void* w
     __syncthreads();
     if (!only_split) {  // (continue_upscale's first step only splits the stored level)
         // interval means (clustering.py:60-83): reduceat sums of w, w*v, v
-        for (int c = threadIdx.x; c < m; c += kThreads) {
-            const int a = sb[c], len = sb[c + 1] - sb[c];
-            double mean = NAN;
-            if (len > 0) {
-                const double sum_w = reduceat_sum([&](int64_t i) { return sw[i]; }, a, len);
-                const double sum_wv = reduceat_sum([&](int64_t i) { return sw[i] * sv[i]; }, a, len);
-                if (sum_w > 0.0) {
-                    mean = sum_wv / sum_w;
-                } else {
-                    const double sum_v = reduceat_sum([&](int64_t i) { return sv[i]; }, a, len);
-                    mean = sum_v / (double)len;
-                }
-            }
-            means[c] = mean;
-        }
+        for (int c = threadIdx.x; c < m; c += kThreads) means[c] = interval_mean(sv, sw, sb[c], sb[c + 1] - sb[c]);
         __syncthreads();
         // empty intervals (quantizer.py:244-259): seed -> copy the previous column;
         // otherwise -> the parent's float64 centroid
@@ -596,6 +593,36 @@ __global__ void sse_levels_kernel(const double* __restrict__ w, const double* __
     sse[r] = pairwise_sum(term, 0, n);
 }
 
+// cluster_rows + the seed centroids (clustering.py:204-227, quantizer.py:224-259,
+// kmeans_1d_weighted quantizer.py:122-157) for any cluster count k: the DP
+// bounds of every row, float64 interval means with empty trailing intervals
+// copying the previous column, and the interval index of every element in the
+// row's original order.  One CTA per row.
+__global__ void __launch_bounds__(kThreads) cluster_out_kernel(int rows, Ws W, void* ws, int k,
+                                                               const int64_t* __restrict__ order,
+                                                               int* __restrict__ bounds_out,
+                                                               double* __restrict__ means_out,
+                                                               int* __restrict__ codes_out) {
+    const int r = blockIdx.x;
+    if (r >= rows) return;
+    const int n = W.n;
+    const double* sv = slice<double>(ws, W, r, W.off_sv);
+    const double* sw = slice<double>(ws, W, r, W.off_sw);
+    const int* b = slice<int>(ws, W, r, W.off_bounds);
+    double* mr = means_out + (int64_t)r * k;
+    for (int c = threadIdx.x; c <= k; c += kThreads) bounds_out[(int64_t)r * (k + 1) + c] = b[c];
+    for (int c = threadIdx.x; c < k; c += kThreads) mr[c] = interval_mean(sv, sw, b[c], b[c + 1] - b[c]);
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int c = 1; c < k; ++c)
+            if (isnan(mr[c])) mr[c] = mr[c - 1];
+    if (codes_out) {
+        const int64_t* orr = order + (int64_t)r * n;
+        for (int c = threadIdx.x >> 5; c < k; c += kThreads / 32)
+            for (int p = b[c] + (threadIdx.x & 31); p < b[c + 1]; p += 32) codes_out[(int64_t)r * n + orr[p]] = c;
+    }
+}
+
 int finish() { return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA; }
 
 }  // namespace
@@ -666,5 +693,30 @@ extern "C" int apb_quant_sse_levels(const double* weights, const double* sens, c
     if (k < 1 || k > kMaxLevelBits || shift < 0 || shift > 7) return APB_ERR_PARAM;
     sse_levels_kernel<<<(rows + 127) / 128, 128, 0, (cudaStream_t)stream>>>(weights, sens, codes, shift, table_k, k,
                                                                             rows, n, sse);
+    return finish();
+}
+
+// Workspace for apb_quant_cluster: the DP keeps k - 2 argmin rows per channel.
+extern "C" int64_t apb_quant_cluster_workspace(int rows, int n, int k) {
+    if (rows <= 0 || n <= 0 || k < 1 || k > 4096) return -1;
+    int nb = 1;
+    while ((1 << nb) < k) ++nb;  // bounds area of 2^nb + 1 entries
+    return (int64_t)rows * (int64_t)Ws(n, k, nb).row_bytes;
+}
+
+extern "C" int apb_quant_cluster(const double* weights, const double* sens, const int64_t* order, int rows, int n,
+                                 int k, int* bounds, double* means, int* codes, void* workspace,
+                                 int64_t workspace_bytes, void* stream) {
+    if (!weights || !sens || !order || !bounds || !means || !workspace) return APB_ERR_PARAM;
+    const int64_t need = apb_quant_cluster_workspace(rows, n, k);
+    if (need < 0) return rows <= 0 || n <= 0 ? APB_ERR_SHAPE : APB_ERR_PARAM;
+    if (workspace_bytes < need || ((uintptr_t)workspace & 15)) return APB_ERR_PARAM;
+    int nb = 1;
+    while ((1 << nb) < k) ++nb;
+    cudaStream_t st = (cudaStream_t)stream;
+    const Ws W(n, k, nb);
+    prefix_kernel<<<(rows + 127) / 128, 128, 0, st>>>(weights, sens, order, rows, W, workspace);
+    seed_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace);
+    cluster_out_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, k, order, bounds, means, codes);
     return finish();
 }

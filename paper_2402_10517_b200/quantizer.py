@@ -199,3 +199,138 @@ def continue_upscale(weights, sens, layer, new_n_max: int, *, row_block: int | N
     return AnyPrecisionLayer(n_min=layer.n_min, n_max=new_n_max, codes=conv(codes),
                              centroid_tables={k: conv(t) for k, t in all_tables.items()}, shape=(rows, n),
                              channel_sse={k: conv(t) for k, t in all_sse.items()})
+
+
+# ---- the rest of the reference quantizer module (quantizer.py:31-72, 122-307) ----
+
+class SensitivityMap:
+    """Per-weight non-negative importance, same shape as the weight matrix
+    (quantizer.py:31-47)."""
+
+    def __init__(self, values, fallback: bool = False):
+        self.values = np.asarray(values, dtype=np.float64)
+        self.fallback = fallback
+        if self.values.ndim != 2:
+            raise ShapeError("sensitivity map must be 2-D")
+        if np.any(self.values < 0):
+            raise ParameterError("sensitivity values must be non-negative")
+
+    @classmethod
+    def uniform(cls, shape, fallback: bool = False) -> "SensitivityMap":
+        return cls(np.ones(shape, dtype=np.float64), fallback=fallback)
+
+
+class ChannelQuantization:
+    """One channel's codes and sorted float64 centroids at one bit-width
+    (quantizer.py:50-72)."""
+
+    def __init__(self, bit_width: int, codes, centroids):
+        self.bit_width = bit_width
+        self.codes = np.asarray(codes)
+        self.centroids = np.asarray(centroids, dtype=np.float64)
+        k = bit_width
+        if not MIN_BITS <= k <= MAX_BITS:
+            raise ParameterError(f"bit width {k} outside [{MIN_BITS}, {MAX_BITS}]")
+        if self.centroids.shape != (1 << k,):
+            raise ShapeError(f"expected {1 << k} centroids for {k}-bit channel, got {self.centroids.shape}")
+        if self.codes.size and (self.codes.min() < 0 or self.codes.max() >= (1 << k)):
+            raise ParameterError("codes out of range for bit width")
+
+    def dequantized(self) -> np.ndarray:
+        return self.centroids[self.codes]
+
+
+class KMeans1DResult(tuple):
+    """(centroids (k,) float64, assignments (n,) int64, padded bool) -- the
+    reference's NamedTuple (clustering.py:25-28)."""
+
+    def __new__(cls, centroids, assignments, padded):
+        return super().__new__(cls, (centroids, assignments, padded))
+
+    centroids = property(lambda self: self[0])
+    assignments = property(lambda self: self[1])
+    padded = property(lambda self: self[2])
+
+
+def estimate_sensitivity_diag(gradient_samples, shape=None) -> SensitivityMap:
+    """Elementwise mean of squared gradient samples (quantizer.py:160-187):
+    host-side statistics of the calibration gradients, same fallbacks."""
+    samples = [np.asarray(g, dtype=np.float64) for g in gradient_samples]
+    if not samples:
+        if shape is None:
+            raise ParameterError("empty sample list needs an explicit shape for the fallback")
+        log.warning("no gradient samples; using uniform sensitivity")
+        return SensitivityMap.uniform(shape, fallback=True)
+    shape = samples[0].shape
+    for g in samples[1:]:
+        if g.shape != shape:
+            raise ShapeError("gradient samples must share one shape")
+    acc = np.zeros(shape, dtype=np.float64)
+    for g in samples:
+        acc += g * g
+    acc /= len(samples)
+    dead = ~np.any(acc > 0, axis=1)
+    if np.any(dead):
+        log.warning("uniform sensitivity fallback for %d all-zero channel(s)", dead.sum())
+        acc[dead] = 1.0
+        return SensitivityMap(acc, fallback=True)
+    return SensitivityMap(acc)
+
+
+def _cluster_device(torch, w, s, k: int):
+    """apb_quant_cluster over the rows of (w, s): bounds, float64 means, codes."""
+    from ._lib import check, load
+
+    lib = load()
+    rows, n = w.shape
+    if k > 4096:
+        raise ParameterError(f"cluster count {k} above the device limit 4096")
+    order = torch.sort(w + 0.0, dim=1, stable=True).indices.contiguous()
+    bounds = torch.empty(rows, k + 1, dtype=torch.int32, device="cuda")
+    means = torch.empty(rows, k, dtype=torch.float64, device="cuda")
+    codes = torch.empty(rows, n, dtype=torch.int32, device="cuda")
+    ws = torch.empty(lib.apb_quant_cluster_workspace(rows, n, k), dtype=torch.uint8, device="cuda")
+    P = dev.ptr
+    check(lib.apb_quant_cluster(P(w), P(s), P(order), rows, n, k, P(bounds), P(means), P(codes), P(ws),
+                                ws.numel(), dev.stream_ptr()), "apb_quant_cluster")
+    return bounds, means, codes
+
+
+def kmeans_1d_weighted(values, weights, k: int) -> KMeans1DResult:
+    """Globally optimal weighted k-means of a 1-D array (quantizer.py:122-157) on
+    the GPU: same validation, same partition (smallest leading cluster on ties),
+    empty clusters duplicate the largest real centroid."""
+    values = np.asarray(values, dtype=np.float64)
+    weights = np.asarray(weights, dtype=np.float64)
+    if values.ndim != 1 or values.size == 0:
+        raise ShapeError("values must be a non-empty 1-D array")
+    if weights.shape != values.shape:
+        raise ShapeError(f"weights shape {weights.shape} != values shape {values.shape}")
+    if k < 1:
+        raise ParameterError(f"k must be >= 1, got {k}")
+    if np.any(weights < 0):
+        raise ParameterError("weights must be non-negative")
+    if weights.sum() <= 0:
+        raise ParameterError("total weight must be positive")
+    torch = dev.require_cuda()
+    w = torch.from_numpy(values[None, :].copy()).cuda()
+    s = torch.from_numpy(weights[None, :].copy()).cuda()
+    _, means, codes = _cluster_device(torch, w, s, k)
+    distinct = int(np.count_nonzero(np.diff(np.sort(values)) > 0)) + 1
+    return KMeans1DResult(means[0].cpu().numpy(), codes[0].cpu().numpy().astype(np.int64), bool(distinct < k))
+
+
+def quantize_seed(weights, sens, n1: int, *, row_block: int = 64) -> list:
+    """Every output channel quantized to n1 bits independently by exact weighted
+    k-means with k = 2^n1 (quantizer.py:281-307), on the GPU."""
+    weights = np.asarray(weights, dtype=np.float64) if not dev.is_tensor(weights) else weights
+    if len(weights.shape) != 2:
+        raise ShapeError("weight matrix must be 2-D")
+    if not MIN_BITS <= n1 <= MAX_BITS:
+        raise ParameterError(f"seed bit-width {n1} outside [{MIN_BITS}, {MAX_BITS}]")
+    torch = dev.require_cuda()
+    w = _to_device_f64(torch, weights).contiguous()
+    s = _coerce_sensitivity(torch, w, sens)
+    _, means, codes = _cluster_device(torch, w, s, 1 << n1)
+    means, codes = means.cpu().numpy(), codes.cpu().numpy().astype(np.int64)
+    return [ChannelQuantization(n1, codes[r], means[r]) for r in range(w.shape[0])]

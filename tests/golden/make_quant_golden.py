@@ -94,6 +94,39 @@ def main():
         out[f"cont/table{k}"] = ext.centroid_tables[k]
         out[f"cont/sse{k}"] = ext.channel_sse[k]
     out["cont/bad_codes"] = rng.integers(0, 32, size=(9, 640), dtype=np.uint8)
+    # quantize_seed / kmeans_1d_weighted (quantizer.py:122-157, 281-307)
+    from anyprec.quantizer import SensitivityMap, kmeans_1d_weighted, quantize_seed  # noqa: E402
+
+    seeds = {
+        "sign": (np.sign(rng.standard_normal((3, 40))) * 2.5, None, 2),
+        "eight": (rng.permutation(np.arange(8.0))[None, :].repeat(2, 0), None, 3),
+        "rand": (rng.standard_normal((5, 300)), rng.random((5, 300)), 2),
+        "dead": (rng.standard_normal((4, 100)), np.vstack([rng.random((3, 100)), np.zeros((1, 100))]), 3),
+        "tiny": (np.array([[1.0], [2.0]]), None, 2),
+    }
+    for name, (sw_, ss_, n1) in seeds.items():
+        cqs = quantize_seed(sw_, SensitivityMap(ss_) if ss_ is not None else None, n1)
+        out[f"seed/{name}/weights"] = sw_
+        if ss_ is not None:
+            out[f"seed/{name}/sens"] = ss_
+        out[f"seed/{name}/n1"] = np.array(n1)
+        out[f"seed/{name}/codes"] = np.stack([c.codes for c in cqs])
+        out[f"seed/{name}/centroids"] = np.stack([c.centroids for c in cqs])
+    kms = [("k1", 1), ("k3", 3), ("k5", 5), ("k7", 7), ("k12", 12)]
+    for name, k in kms:
+        v = rng.standard_normal(257) * 3.0
+        wt = rng.random(257)
+        res = kmeans_1d_weighted(v, wt, k)
+        out[f"km/{name}/values"], out[f"km/{name}/weights"], out[f"km/{name}/k"] = v, wt, np.array(k)
+        out[f"km/{name}/centroids"], out[f"km/{name}/assignments"] = res.centroids, res.assignments
+        out[f"km/{name}/padded"] = np.array(res.padded)
+    v = np.array([1.0, 1.0, 2.0, 2.0, 2.0])  # fewer distinct values than clusters
+    res = kmeans_1d_weighted(v, np.ones(5), 4)
+    out["km/pad/values"], out["km/pad/weights"], out["km/pad/k"] = v, np.ones(5), np.array(4)
+    out["km/pad/centroids"], out["km/pad/assignments"] = res.centroids, res.assignments
+    out["km/pad/padded"] = np.array(res.padded)
+    out["km_cases"] = np.array([n for n, _ in kms] + ["pad"])
+    out["seed_cases"] = np.array(list(seeds))
     try:
         continue_upscale(w, s, type(base)(n_min=3, n_max=5, codes=out["cont/bad_codes"],
                                           centroid_tables=base.centroid_tables, shape=base.shape), 8)

@@ -130,3 +130,37 @@ def test_continue_upscale_bit_exact_vs_reference():
         continue_upscale(w, s, bad, 8)
     with pytest.raises(ParameterError):
         continue_upscale(w, s, base, 5)
+
+
+def test_quantize_seed_and_kmeans_bit_exact_vs_reference():
+    """quantize_seed (quantizer.py:281-307: sign pattern, 8 distinct values,
+    SensitivityMap weights, a dead channel, fewer values than clusters) and
+    kmeans_1d_weighted (quantizer.py:122-157 at k = 1, 3, 5, 7, 12 and a padded
+    case): codes / assignments and float64 centroids bit-identical."""
+    from paper_2402_10517_b200.errors import ParameterError, ShapeError
+    from paper_2402_10517_b200.quantizer import SensitivityMap, kmeans_1d_weighted, quantize_seed
+
+    z = np.load(GOLDEN)
+    for name in z["seed_cases"]:
+        name = str(name)
+        w = z[f"seed/{name}/weights"]
+        s = SensitivityMap(z[f"seed/{name}/sens"]) if f"seed/{name}/sens" in z else None
+        cqs = quantize_seed(w, s, int(z[f"seed/{name}/n1"]))
+        np.testing.assert_array_equal(np.stack([c.codes for c in cqs]), z[f"seed/{name}/codes"], err_msg=name)
+        np.testing.assert_array_equal(np.stack([c.centroids for c in cqs]).view(np.uint64),
+                                      z[f"seed/{name}/centroids"].view(np.uint64), err_msg=name)
+    for name in z["km_cases"]:
+        name = str(name)
+        res = kmeans_1d_weighted(z[f"km/{name}/values"], z[f"km/{name}/weights"], int(z[f"km/{name}/k"]))
+        np.testing.assert_array_equal(res.assignments, z[f"km/{name}/assignments"], err_msg=name)
+        np.testing.assert_array_equal(res.centroids.view(np.uint64), z[f"km/{name}/centroids"].view(np.uint64),
+                                      err_msg=name)
+        assert res.padded == bool(z[f"km/{name}/padded"]), name
+    with pytest.raises(ShapeError):
+        quantize_seed(np.ones((2, 4)), np.ones((2, 5)), 2)
+    with pytest.raises(ParameterError):
+        quantize_seed(np.ones((1, 4)), None, 1)
+    with pytest.raises(ParameterError):
+        kmeans_1d_weighted(np.ones(4), np.zeros(4), 2)
+    with pytest.raises(ShapeError):
+        kmeans_1d_weighted(np.ones((2, 2)), np.ones((2, 2)), 2)
