@@ -299,6 +299,19 @@ int apb_quant_continue(const double* weights, const double* sens, const int64_t*
  * ([rows][k], an empty interval copies the previous column) and, if codes is
  * not NULL, each element's interval index in original order ([rows][n]).
  * sens must be coerced by the caller; order is the stable argsort. */
+/* upscale (quantizer.py:310-367), one bit more for each row: value-contiguous
+ * codes (in each row's sorted order) go through the split kernels with the
+ * float64 centroids `parents` [rows][2^k0] (workspace:
+ * apb_quant_workspace(rows, n, 2, k0 + 1); *bad |= 1 if some row is not
+ * contiguous); other codes through apb_quant_upscale_general (gorder = stable
+ * sort by (code, value), scratch >= rows * (2n + 3(n + 2^k0 + 1)) doubles).
+ * Outputs: codes [rows][n] uint8 and float64 centroids [rows][2^(k0+1)]. */
+int apb_quant_upscale(const double* weights, const double* sens, const int64_t* order, const uint8_t* codes_in,
+                      const double* parents, int rows, int n, int k0, uint8_t* codes, double* means, int* bad,
+                      void* workspace, int64_t workspace_bytes, void* stream);
+int apb_quant_upscale_general(const double* weights, const double* sens, const int64_t* gorder,
+                              const uint8_t* codes_in, const double* parents, int rows, int n, int k0,
+                              uint8_t* codes, double* means, double* scratch, void* stream);
 int64_t apb_quant_cluster_workspace(int rows, int n, int k);
 int apb_quant_cluster(const double* weights, const double* sens, const int64_t* order, int rows, int n, int k,
                       int* bounds, double* means, int* codes, void* workspace, int64_t workspace_bytes,

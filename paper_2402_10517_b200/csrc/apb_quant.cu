@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kThreads) level_kernel(int rows, Ws W, void* w
         __syncthreads();
         for (int c = threadIdx.x; c < m; c += kThreads) {
             const __half h = __double2half(means[c]);
-            table[(int64_t)r * m + c] = __half_as_ushort(h);
+            if (table) table[(int64_t)r * m + c] = __half_as_ushort(h);
             t64[c] = (double)__half2float(h);
             parents[c] = means[c];  // the next level's parents
         }
@@ -476,9 +476,9 @@ __global__ void __launch_bounds__(kThreads) level_kernel(int rows, Ws W, void* w
                             --sp;
                         }
                     }
-                    sse[r] = ret;
+                    if (sse) sse[r] = ret;
                 }
-            } else if (threadIdx.x == 0) {
+            } else if (threadIdx.x == 0 && sse) {
                 sse[r] = pairwise_sum(term, 0, n);
             }
         }
@@ -544,7 +544,8 @@ __global__ void __launch_bounds__(kThreads) bounds_from_codes_kernel(int rows, W
                                                                      const uint8_t* __restrict__ codes, int k0,
                                                                      const int64_t* __restrict__ order,
                                                                      const uint16_t* __restrict__ table,
-                                                                     int* __restrict__ bad) {
+                                                                     int* __restrict__ bad,
+                                                                     const double* __restrict__ parents64) {
     const int r = blockIdx.x;
     if (r >= rows) return;
     const int n = W.n, m = 1 << k0;
@@ -572,7 +573,8 @@ __global__ void __launch_bounds__(kThreads) bounds_from_codes_kernel(int rows, W
         }
     }
     for (int c = threadIdx.x; c < m; c += kThreads)
-        parents[c] = (double)__half2float(__ushort_as_half(table[(int64_t)r * m + c]));
+        parents[c] = parents64 ? parents64[(int64_t)r * m + c]
+                               : (double)__half2float(__ushort_as_half(table[(int64_t)r * m + c]));
 }
 
 // continue_upscale's error record of the EXISTING levels (quantizer.py:499-503):
@@ -623,6 +625,108 @@ __global__ void __launch_bounds__(kThreads) cluster_out_kernel(int rows, Ws W, v
     }
 }
 
+// _upscale_general (quantizer.py:344-367): codes that are not value-contiguous.
+// Every cluster b is split by its own exact weighted 2-means
+// (kmeans_1d_weighted of its members, weights -> 1 when they sum to 0): the
+// row arrives sorted by (code, value) (ties by position), each warp takes whole
+// clusters, builds their fresh prefix sums from 0 (as the per-cluster k-means
+// does), scans the k = 2 DP's last layer and writes codes 2b / 2b+1 and the two
+// centroids; fewer than two distinct members -> all 2b, both centroids = their
+// mean; an empty cluster -> both = the parent centroid.
+__global__ void __launch_bounds__(kThreads) upscale_general_kernel(
+    const double* __restrict__ w, const double* __restrict__ s, const int64_t* __restrict__ gorder,
+    const uint8_t* __restrict__ codes_in, const double* __restrict__ parents, int rows, int n, int k0,
+    uint8_t* __restrict__ codes_out, double* __restrict__ means_out, double* __restrict__ scratch) {
+    const int r = blockIdx.x;
+    if (r >= rows) return;
+    const int m = 1 << k0, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t* go = gorder + (int64_t)r * n;
+    const double* wr = w + (int64_t)r * n;
+    const double* sr = s + (int64_t)r * n;
+    const uint8_t* cr = codes_in + (int64_t)r * n;
+    // scratch per row: sv, sw [n] and pw / pwv / pwv2 [n + m + 1] (cluster b's prefix at start_b + b)
+    const int64_t stride = 2 * (int64_t)n + 3 * ((int64_t)n + m + 1);
+    double* sv = scratch + (int64_t)r * stride;
+    double* sw = sv + n;
+    double* pw = sw + n;
+    double* pwv = pw + (n + m + 1);
+    double* pwv2 = pwv + (n + m + 1);
+    __shared__ int start[kMaxIntervals + 1];
+    if (threadIdx.x == 0) {  // clusters are contiguous in (code, value) order
+        int c = 0;
+        for (int p = 0; p < n; ++p)
+            while (c <= (int)cr[go[p]]) start[c++] = p;
+        while (c <= m) start[c++] = n;
+    }
+    __syncthreads();
+    for (int b = warp; b < m; b += kThreads / 32) {
+        const int a = start[b], len = start[b + 1] - a;
+        double* outm = means_out + (int64_t)r * 2 * m;
+        if (len == 0) {
+            if (lane == 0) outm[2 * b] = outm[2 * b + 1] = parents[(int64_t)r * m + b];
+            continue;
+        }
+        // members in value order, weights (or ones when they sum to 0)
+        bool any_w = false;
+        for (int i = lane; i < len; i += 32) any_w |= sr[go[a + i]] > 0.0;
+        any_w = __any_sync(0xffffffffu, any_w);
+        for (int i = lane; i < len; i += 32) {
+            const int64_t o = go[a + i];
+            sv[a + i] = wr[o];
+            sw[a + i] = any_w ? sr[o] : 1.0;
+        }
+        __syncwarp();
+        const int pb = a + b;  // this cluster's prefix slice
+        int distinct = 1;
+        if (lane == 0) {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+            pw[pb] = pwv[pb] = pwv2[pb] = 0.0;
+            for (int i = 0; i < len; ++i) {
+                const double v = sv[a + i], x = sw[a + i], xv = x * v;
+                a0 += x;
+                a1 += xv;
+                a2 += xv * v;
+                pw[pb + i + 1] = a0;
+                pwv[pb + i + 1] = a1;
+                pwv2[pb + i + 1] = a2;
+                if (i > 0 && v - sv[a + i - 1] > 0.0) ++distinct;
+            }
+        }
+        distinct = __shfl_sync(0xffffffffu, distinct, 0);
+        __syncwarp();
+        int split = len;  // padded: every member in the low child
+        if (distinct >= 2) {
+            const double e0 = pw[pb + len], e1 = pwv[pb + len], e2 = pwv2[pb + len];
+            double v = INFINITY;
+            int i = INT32_MAX;
+            bool first = true;
+            for (int j = 1 + lane; j <= len - 1; j += 32) {
+                const double d1 = pwv2[pb + j] - pwv[pb + j] * pwv[pb + j] / fmax(pw[pb + j], kTiny);
+                const double dw = e0 - pw[pb + j], dwv = e1 - pwv[pb + j], dwv2 = e2 - pwv2[pb + j];
+                double c = dwv2 - dwv * dwv / fmax(dw, kTiny);
+                c += d1;
+                if (first) {
+                    v = c;
+                    i = j;
+                    first = false;
+                } else {
+                    argmin_merge(v, i, c, j);
+                }
+            }
+            warp_argmin(v, i);
+            split = i;
+        }
+        if (lane == 0) {
+            const double lo = interval_mean(sv + a, sw + a, 0, split);
+            const double hi = split < len ? interval_mean(sv + a, sw + a, split, len - split) : lo;
+            outm[2 * b] = lo;
+            outm[2 * b + 1] = hi;
+        }
+        for (int i2 = lane; i2 < len; i2 += 32)
+            codes_out[(int64_t)r * n + go[a + i2]] = (uint8_t)(2 * b + (i2 >= split ? 1 : 0));
+    }
+}
+
 int finish() { return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA; }
 
 }  // namespace
@@ -670,7 +774,8 @@ extern "C" int apb_quant_continue(const double* weights, const double* sens, con
     cudaStream_t st = (cudaStream_t)stream;
     const Ws W(n, 1 << 2, new_n_max);  // no DP here
     prefix_kernel<<<(rows + 127) / 128, 128, 0, st>>>(weights, sens, order, rows, W, workspace);
-    bounds_from_codes_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, codes_in, k0, order, table_k0, bad);
+    bounds_from_codes_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, codes_in, k0, order, table_k0, bad,
+                                                         nullptr);
     level_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, k0, 0, 0, 1, 1, nullptr, nullptr, nullptr, nullptr,
                                              order);
     int cur = 1;
@@ -718,5 +823,46 @@ extern "C" int apb_quant_cluster(const double* weights, const double* sens, cons
     prefix_kernel<<<(rows + 127) / 128, 128, 0, st>>>(weights, sens, order, rows, W, workspace);
     seed_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace);
     cluster_out_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, k, order, bounds, means, codes);
+    return finish();
+}
+
+// upscale (quantizer.py:310-341), value-contiguous codes: the k0-level bounds
+// from the codes, the channel's float64 centroids as parents, one split, the
+// new level's float64 means (means [rows][2^(k0+1)]) and codes.
+extern "C" int apb_quant_upscale(const double* weights, const double* sens, const int64_t* order,
+                                 const uint8_t* codes_in, const double* parents, int rows, int n, int k0,
+                                 uint8_t* codes, double* means, int* bad, void* workspace, int64_t workspace_bytes,
+                                 void* stream) {
+    if (!weights || !sens || !order || !codes_in || !parents || !codes || !means || !bad || !workspace)
+        return APB_ERR_PARAM;
+    if (rows <= 0 || n <= 0) return APB_ERR_SHAPE;
+    if (k0 < 1 || k0 >= kMaxLevelBits) return APB_ERR_PARAM;
+    const int64_t need = apb_quant_workspace(rows, n, 2, k0 + 1);
+    if (workspace_bytes < need || ((uintptr_t)workspace & 15)) return APB_ERR_PARAM;
+    cudaStream_t st = (cudaStream_t)stream;
+    const Ws W(n, 1 << 2, k0 + 1);
+    prefix_kernel<<<(rows + 127) / 128, 128, 0, st>>>(weights, sens, order, rows, W, workspace);
+    bounds_from_codes_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, codes_in, k0, order, nullptr, bad, parents);
+    level_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, k0, 0, 0, 1, 1, nullptr, nullptr, nullptr, nullptr,
+                                             order);
+    level_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, k0 + 1, 1, 0, 0, 0, nullptr, nullptr, nullptr, codes,
+                                             order);
+    const size_t mb = sizeof(double) << (k0 + 1);
+    if (cudaMemcpy2DAsync(means, mb, static_cast<char*>(workspace) + W.off_parents, W.row_bytes, mb, rows,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return APB_ERR_CUDA;
+    return finish();
+}
+
+// _upscale_general (quantizer.py:344-367): gorder = each row's stable sort by
+// (code, value); scratch >= rows * (2n + 3(n + 2^k0 + 1)) doubles.
+extern "C" int apb_quant_upscale_general(const double* weights, const double* sens, const int64_t* gorder,
+                                         const uint8_t* codes_in, const double* parents, int rows, int n, int k0,
+                                         uint8_t* codes, double* means, double* scratch, void* stream) {
+    if (!weights || !sens || !gorder || !codes_in || !parents || !codes || !means || !scratch) return APB_ERR_PARAM;
+    if (rows <= 0 || n <= 0) return APB_ERR_SHAPE;
+    if (k0 < 1 || k0 >= kMaxLevelBits) return APB_ERR_PARAM;
+    upscale_general_kernel<<<rows, kThreads, 0, (cudaStream_t)stream>>>(weights, sens, gorder, codes_in, parents, rows,
+                                                                        n, k0, codes, means, scratch);
     return finish();
 }

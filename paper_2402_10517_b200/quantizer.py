@@ -334,3 +334,48 @@ def quantize_seed(weights, sens, n1: int, *, row_block: int = 64) -> list:
     _, means, codes = _cluster_device(torch, w, s, 1 << n1)
     means, codes = means.cpu().numpy(), codes.cpu().numpy().astype(np.int64)
     return [ChannelQuantization(n1, codes[r], means[r]) for r in range(w.shape[0])]
+
+
+def upscale(cq: ChannelQuantization, row, sens) -> ChannelQuantization:
+    """Split every cluster of one channel into two (quantizer.py:310-367) on the
+    GPU: value-contiguous codes go through the split kernels with the channel's
+    float64 centroids as parents; any other code assignment through the
+    per-cluster 2-means kernel (the reference's _upscale_general semantics:
+    zero-weight clusters weighted uniformly, single-valued clusters kept whole,
+    empty clusters duplicating the parent)."""
+    from ._lib import check, load
+
+    row = np.asarray(row, dtype=np.float64)
+    sens = np.asarray(sens, dtype=np.float64)
+    if row.shape != cq.codes.shape or sens.shape != row.shape:
+        raise ShapeError("row/sensitivity length does not match the channel codes")
+    if cq.bit_width >= MAX_BITS:
+        raise ParameterError(f"cannot upscale past {MAX_BITS} bits")
+    if not np.all(np.isfinite(row)):
+        raise ParameterError("weights must be finite")
+    if not np.all(np.isfinite(sens)):
+        raise ParameterError("sensitivities must be finite")
+    if np.any(sens < 0):
+        raise ParameterError("sensitivity values must be non-negative")
+    torch = dev.require_cuda()
+    lib, P, st = load(), dev.ptr, dev.stream_ptr()
+    n, k0 = row.size, cq.bit_width
+    w = torch.from_numpy(row[None, :].copy()).cuda()
+    s = torch.from_numpy(sens[None, :].copy()).cuda()
+    codes_in = torch.from_numpy(np.asarray(cq.codes).astype(np.uint8)[None, :].copy()).cuda()
+    parents = torch.from_numpy(np.ascontiguousarray(cq.centroids, dtype=np.float64)[None, :]).cuda()
+    codes = torch.empty(1, n, dtype=torch.uint8, device="cuda")
+    means = torch.empty(1, 2 << k0, dtype=torch.float64, device="cuda")
+    order = torch.sort(w + 0.0, dim=1, stable=True).indices.contiguous()
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(lib.apb_quant_workspace(1, n, 2, k0 + 1), dtype=torch.uint8, device="cuda")
+    check(lib.apb_quant_upscale(P(w), P(s), P(order), P(codes_in), P(parents), 1, n, k0, P(codes), P(means),
+                                P(bad), P(ws), ws.numel(), st), "apb_quant_upscale")
+    if int(bad.item()):  # codes are not value-contiguous: per-cluster 2-means
+        by_code = torch.sort(codes_in.gather(1, order).to(torch.int32), dim=1, stable=True).indices
+        gorder = order.gather(1, by_code).contiguous()
+        scratch = torch.empty(2 * n + 3 * (n + (1 << k0) + 1), dtype=torch.float64, device="cuda")
+        check(lib.apb_quant_upscale_general(P(w), P(s), P(gorder), P(codes_in), P(parents), 1, n, k0, P(codes),
+                                            P(means), P(scratch), st), "apb_quant_upscale_general")
+    return ChannelQuantization(k0 + 1, codes[0].cpu().numpy().astype(np.asarray(cq.codes).dtype),
+                               means[0].cpu().numpy())

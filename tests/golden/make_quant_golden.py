@@ -126,6 +126,34 @@ def main():
     out["km/pad/centroids"], out["km/pad/assignments"] = res.centroids, res.assignments
     out["km/pad/padded"] = np.array(res.padded)
     out["km_cases"] = np.array([n for n, _ in kms] + ["pad"])
+    # upscale (quantizer.py:310-367): interval and general paths
+    from anyprec.quantizer import ChannelQuantization, upscale  # noqa: E402
+
+    ups = {}
+    row = rng.standard_normal(200)
+    sens = rng.random(200)
+    ups["contig"] = (quantize_seed(row[None, :], sens[None, :], 2)[0], row, sens)
+    ups["ident"] = (ChannelQuantization(2, np.zeros(4, dtype=np.int64), np.array([1.0, 1.0, 1.0, 1.0])),
+                    np.ones(4), np.ones(4))
+    rowe = np.concatenate([rng.standard_normal(30) - 3, rng.standard_normal(30) + 3])
+    ups["empty"] = (ChannelQuantization(2, np.where(rowe > 0, 3, 0).astype(np.int64), np.array([-3.0, -1.0, 1.0, 3.0])),
+                    rowe, rng.random(60))
+    cq = quantize_seed(row[None, :], sens[None, :], 3)[0]
+    shuffled = ChannelQuantization(3, rng.permutation(cq.codes), cq.centroids)
+    ups["general"] = (shuffled, row, sens)
+    sz = sens.copy()
+    sz[shuffled.codes == 2] = 0.0  # a zero-weight cluster: uniform weights
+    ups["general_zw"] = (shuffled, row, sz)
+    rowd = np.round(rng.standard_normal(90), 1)
+    ups["general_dup"] = (ChannelQuantization(2, rng.integers(0, 3, 90), np.array([-1.0, 0.0, 1.0, 2.0])),
+                          rowd, rng.random(90))  # code 3 empty, duplicates within clusters
+    for name, (cq_, r_, s_) in ups.items():
+        up = upscale(cq_, r_, s_)
+        out[f"up/{name}/codes_in"], out[f"up/{name}/centroids_in"] = np.asarray(cq_.codes), cq_.centroids
+        out[f"up/{name}/bits"] = np.array(cq_.bit_width)
+        out[f"up/{name}/row"], out[f"up/{name}/sens"] = r_, s_
+        out[f"up/{name}/codes"], out[f"up/{name}/centroids"] = up.codes, up.centroids
+    out["up_cases"] = np.array(list(ups))
     out["seed_cases"] = np.array(list(seeds))
     try:
         continue_upscale(w, s, type(base)(n_min=3, n_max=5, codes=out["cont/bad_codes"],

@@ -164,3 +164,45 @@ def test_quantize_seed_and_kmeans_bit_exact_vs_reference():
         kmeans_1d_weighted(np.ones(4), np.zeros(4), 2)
     with pytest.raises(ShapeError):
         kmeans_1d_weighted(np.ones((2, 2)), np.ones((2, 2)), 2)
+
+
+def test_upscale_bit_exact_vs_reference():
+    """upscale (quantizer.py:310-367): the interval path (value-contiguous codes,
+    incl. identical members and an empty cluster) and the per-cluster general
+    path (scrambled codes, a zero-weight cluster, duplicates, an empty cluster)
+    give the reference's codes and float64 centroids bit for bit."""
+    from paper_2402_10517_b200.errors import ParameterError, ShapeError
+    from paper_2402_10517_b200.quantizer import ChannelQuantization, upscale
+
+    z = np.load(GOLDEN)
+    for name in z["up_cases"]:
+        name = str(name)
+        cq = ChannelQuantization(int(z[f"up/{name}/bits"]), z[f"up/{name}/codes_in"], z[f"up/{name}/centroids_in"])
+        up = upscale(cq, z[f"up/{name}/row"], z[f"up/{name}/sens"])
+        assert up.bit_width == cq.bit_width + 1
+        np.testing.assert_array_equal(up.codes, z[f"up/{name}/codes"], err_msg=name)
+        np.testing.assert_array_equal(up.centroids.view(np.uint64), z[f"up/{name}/centroids"].view(np.uint64),
+                                      err_msg=name)
+    cq = ChannelQuantization(2, np.zeros(4, dtype=np.int64), np.zeros(4))
+    with pytest.raises(ShapeError):
+        upscale(cq, np.ones(3), np.ones(3))
+    with pytest.raises(ParameterError):
+        upscale(ChannelQuantization(8, np.zeros(4, dtype=np.int64), np.zeros(256)), np.ones(4), np.ones(4))
+
+
+def test_build_matches_seed_plus_repeated_upscale():
+    """test_quantizer.py:197-210 restated: per channel, quantize_seed then
+    upscale to n_max gives build_any_precision's codes and (rounded) tables."""
+    from paper_2402_10517_b200.quantizer import build_any_precision, quantize_seed, upscale
+
+    rng = np.random.default_rng(8)
+    w = rng.standard_normal((5, 300))
+    s = rng.random((5, 300))
+    layer = build_any_precision(w, s, 2, 5)
+    for r in range(5):
+        cq = quantize_seed(w[r][None, :], s[r][None, :], 2)[0]
+        np.testing.assert_array_equal(cq.centroids.astype(np.float16), layer.centroid_tables[2][r])
+        for k in range(3, 6):
+            cq = upscale(cq, w[r], s[r])
+            np.testing.assert_array_equal(cq.centroids.astype(np.float16), layer.centroid_tables[k][r])
+        np.testing.assert_array_equal(cq.codes, layer.codes[r])
