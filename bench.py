@@ -672,6 +672,17 @@ def _oracle_step(ls, threads: int):
             ora.gemm(planes, cols, k, tables[k], x, nthreads=threads)
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline():
     """The oracle C port on the host: 1 thread, full steps (7 layers x
     k = 3..8) repeated until >= 10 s of CPU work (at most 5)."""
@@ -684,7 +695,7 @@ def cpu_baseline():
     return {"value": round(step_bytes() / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"{steps} full steps (7 layers x k=3..8, the bench workload), 1 thread, "
                       "oracle/anyprec_oracle.c (C port of reference engine.py gemv)",
-            "seconds": round(dt * steps, 2)}
+            "seconds": round(dt * steps, 2), "cpu_model": _cpu_model()}
 
 
 def run_reference(args):
@@ -709,7 +720,7 @@ def run_reference(args):
         "config": {"workload": "llama2-7b decode layer set (configs[1])", "bits": BITS, "batch": 1},
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": f"{steps} full step(s), {threads} threads, oracle/anyprec_oracle.c "
-                                   "(C port of the reference engine.py pipeline)"},
+                                   "(C port of the reference engine.py pipeline)", "cpu_model": _cpu_model()},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
