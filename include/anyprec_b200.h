@@ -312,6 +312,13 @@ int apb_quant_upscale(const double* weights, const double* sens, const int64_t* 
 int apb_quant_upscale_general(const double* weights, const double* sens, const int64_t* gorder,
                               const uint8_t* codes_in, const double* parents, int rows, int n, int k0,
                               uint8_t* codes, double* means, double* scratch, void* stream);
+/* split_boundaries (clustering.py:252-302): rows of sorted values sv with
+ * weights sw ([rows][n], identity = 0..n-1 per row as int64), interval bounds
+ * [rows][2^log2m + 1] -> the 2-means split of every interval
+ * out [rows][2^(log2m+1) + 1] (prefix sums recomputed like _prefix_sums).
+ * Workspace: apb_quant_workspace(rows, n, 2, log2m + 1). */
+int apb_quant_split(const double* sv, const double* sw, const int64_t* identity, int rows, int n, int log2m,
+                    const int* bounds, int* out, void* workspace, int64_t workspace_bytes, void* stream);
 int64_t apb_quant_cluster_workspace(int rows, int n, int k);
 int apb_quant_cluster(const double* weights, const double* sens, const int64_t* order, int rows, int n, int k,
                       int* bounds, double* means, int* codes, void* workspace, int64_t workspace_bytes,

@@ -101,6 +101,7 @@ SIGNATURES = {
     "apb_quant_continue": ([_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I64, _P], _I),
     "apb_quant_upscale": ([_P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _I64, _P], _I),
     "apb_quant_upscale_general": ([_P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P], _I),
+    "apb_quant_split": ([_P, _P, _P, _I, _I, _I, _P, _P, _P, _I64, _P], _I),
     "apb_quant_cluster_workspace": ([_I, _I, _I], _I64),
     "apb_quant_cluster": ([_P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _I64, _P], _I),
     "apb_quant_sse_levels": ([_P, _P, _P, _I, _P, _I, _I, _I, _P, _P], _I),

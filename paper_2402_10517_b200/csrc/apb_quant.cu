@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(kThreads) level_kernel(int rows, Ws W, void* w
         if (lane == 0) {
             nbounds[2 * c] = b0;
             nbounds[2 * c + 1] = s;
-            if (c == m - 1) nbounds[2 * m] = n;
+            if (c == m - 1) nbounds[2 * m] = sb[m];  // out[:, 0::2] = bounds
         }
     }
 }
@@ -864,5 +864,40 @@ extern "C" int apb_quant_upscale_general(const double* weights, const double* se
     if (k0 < 1 || k0 >= kMaxLevelBits) return APB_ERR_PARAM;
     upscale_general_kernel<<<rows, kThreads, 0, (cudaStream_t)stream>>>(weights, sens, gorder, codes_in, parents, rows,
                                                                         n, k0, codes, means, scratch);
+    return finish();
+}
+
+// split_boundaries (clustering.py:252-302) on caller bounds: rows of already
+// sorted (sv, sw) with identity order, their bounds [rows][m+1] (m a power of
+// two <= 256), out [rows][2m+1].
+__global__ void load_bounds_kernel(int rows, Ws W, void* ws, int m, const int* __restrict__ bounds) {
+    const int r = blockIdx.x;
+    if (r >= rows) return;
+    int* b = slice<int>(ws, W, r, W.off_bounds);
+    for (int c = threadIdx.x; c <= m; c += blockDim.x) b[c] = bounds[(int64_t)r * (m + 1) + c];
+}
+__global__ void store_bounds_kernel(int rows, Ws W, void* ws, int m, int* __restrict__ out) {
+    const int r = blockIdx.x;
+    if (r >= rows) return;
+    const int* b = slice<int>(ws, W, r, W.off_bounds) + ((1 << W.n_max) + 1);  // slot 1
+    for (int c = threadIdx.x; c <= 2 * m; c += blockDim.x) out[(int64_t)r * (2 * m + 1) + c] = b[c];
+}
+
+extern "C" int apb_quant_split(const double* sv, const double* sw, const int64_t* identity, int rows, int n,
+                               int log2m, const int* bounds, int* out, void* workspace, int64_t workspace_bytes,
+                               void* stream) {
+    if (!sv || !sw || !identity || !bounds || !out || !workspace) return APB_ERR_PARAM;
+    if (rows <= 0 || n <= 0) return APB_ERR_SHAPE;
+    if (log2m < 0 || log2m >= kMaxLevelBits) return APB_ERR_PARAM;
+    const int64_t need = apb_quant_workspace(rows, n, 2, log2m + 1);
+    if (workspace_bytes < need || ((uintptr_t)workspace & 15)) return APB_ERR_PARAM;
+    cudaStream_t st = (cudaStream_t)stream;
+    const Ws W(n, 1 << 2, log2m + 1);
+    const int m = 1 << log2m;
+    prefix_kernel<<<(rows + 127) / 128, 128, 0, st>>>(sv, sw, identity, rows, W, workspace);
+    load_bounds_kernel<<<rows, 128, 0, st>>>(rows, W, workspace, m, bounds);
+    level_kernel<<<rows, kThreads, 0, st>>>(rows, W, workspace, log2m, 0, 0, 1, 1, nullptr, nullptr, nullptr,
+                                             nullptr, identity);
+    store_bounds_kernel<<<rows, 128, 0, st>>>(rows, W, workspace, m, out);
     return finish();
 }

@@ -154,6 +154,17 @@ def main():
         out[f"up/{name}/row"], out[f"up/{name}/sens"] = r_, s_
         out[f"up/{name}/codes"], out[f"up/{name}/centroids"] = up.codes, up.centroids
     out["up_cases"] = np.array(list(ups))
+    # clustering.cluster_rows / split_boundaries (clustering.py:204-302)
+    from anyprec import clustering as cl  # noqa: E402
+
+    vals = np.vstack([rng.standard_normal(150), np.repeat(rng.standard_normal(3), 50),
+                      np.round(rng.standard_normal(150), 1)])
+    wts = rng.random((3, 150))
+    b, order, sv_, sw_, padded = cl.cluster_rows(vals, wts, 8)
+    pw, pwv, pwv2 = cl._prefix_sums(sv_, sw_)
+    sb = cl.split_boundaries(sv_, sw_, pw, pwv, pwv2, b)
+    out["cl/values"], out["cl/weights"] = vals, wts
+    out["cl/bounds"], out["cl/order"], out["cl/padded"], out["cl/split"] = b, order, padded, sb
     out["seed_cases"] = np.array(list(seeds))
     try:
         continue_upscale(w, s, type(base)(n_min=3, n_max=5, codes=out["cont/bad_codes"],

@@ -206,3 +206,18 @@ def test_build_matches_seed_plus_repeated_upscale():
             cq = upscale(cq, w[r], s[r])
             np.testing.assert_array_equal(cq.centroids.astype(np.float16), layer.centroid_tables[k][r])
         np.testing.assert_array_equal(cq.codes, layer.codes[r])
+
+
+def test_clustering_mirror_vs_reference():
+    """clustering.cluster_rows / split_boundaries (clustering.py:204-302) on rows
+    with many, 3 (padded) and repeated values: bounds, order, padded flags and
+    the 2-means splits equal the reference's."""
+    from paper_2402_10517_b200 import clustering
+
+    z = np.load(GOLDEN)
+    b, order, sv, sw, padded = clustering.cluster_rows(z["cl/values"], z["cl/weights"], 8)
+    np.testing.assert_array_equal(b, z["cl/bounds"])
+    np.testing.assert_array_equal(order, z["cl/order"])
+    np.testing.assert_array_equal(padded, z["cl/padded"])
+    split = clustering.split_boundaries(sv, sw, None, None, None, b)
+    np.testing.assert_array_equal(split, z["cl/split"])
