@@ -17,6 +17,7 @@ import numpy as np
 
 from . import _device as dev
 from .errors import ParameterError
+from .quantizer import KMeans1DResult  # noqa: F401  (defined in clustering.py in the reference)
 
 
 def cluster_rows(values, weights, k: int):

@@ -23,16 +23,17 @@ import numpy as np
 
 from . import _device as dev
 from ._lib import APB_DTYPE_F16, APB_DTYPE_F32, check, int64_array, int_array, load, ptr_array
-from .bitplane import (
+from .bitplane import (  # noqa: F401  (pack_bitplanes: re-exported like the reference's engine module)
     LANES,
     LAYOUT_PERMUTED,
     TILE_WEIGHTS,
     BitplaneTensor,
+    pack_bitplanes,
     pack_permuted,
     permute_layout,
 )
 from .errors import ParameterError, ShapeError
-from .layer import supported_bits
+from .layer import AnyPrecisionLayer, supported_bits  # noqa: F401  (re-exported like the reference)
 
 # Op budget of the REFERENCE's delta-swap network (engine.py:44-45); kept for
 # API parity.  The kernels use the select-form networks of csrc/apb_common.cuh.
