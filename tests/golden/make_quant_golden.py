@@ -10,8 +10,11 @@ for every k, float64 channel_sse for every k, level codes).  The cases cover
 random rows with zero-sensitivity entries and a dead (all-zero) row,
 low-distinct rows (k_eff < 2^n_min, padded tables, unsplittable clusters),
 duplicates, -0.0 / +0.0 ties, n_min = 2, and a row wider than 8192 (deep
-pairwise-summation tree); plus continue_upscale of a 3..5-bit layer to 8 bits
-("cont/*") and its error message for codes that are not value-contiguous.  Nothing at test or bench time reads /root/reference.
+pairwise-summation tree), n_min == n_max and a 32-cluster seed; plus
+continue_upscale of a 3..5-bit layer to 8 bits ("cont/*") and its error message
+for codes that are not value-contiguous; quantize_seed ("seed/*") and
+kmeans_1d_weighted at non-power-of-two k ("km/*"); upscale on both of its paths
+("up/*"); clustering.cluster_rows / split_boundaries ("cl/*").  Nothing at test or bench time reads /root/reference.
 """
 
 from __future__ import annotations
