@@ -184,3 +184,25 @@ def test_embed_rms_and_argmax():
         check(lib.apb_argmax_f16(P(x), n, P(o), st), "apb_argmax_f16")
         torch.cuda.synchronize()
         assert int(o) == (n // 3 if n > 10 else 0), (n, int(o))
+
+
+def test_decode_step_llama7b_block_shapes():
+    """Two decoder blocks at the real Llama-2-7B shapes (hidden 4096,
+    intermediate 11008, 32 heads, context 256): the folded RMSNorm / GLU
+    epilogues and the attention kernel at production sizes, against the same
+    fp32 reference built from the dequantized weights."""
+    import torch
+
+    from paper_2402_10517_b200 import engine
+    from paper_2402_10517_b200.decode import DecodeModel, LlamaConfig
+
+    cfg = LlamaConfig(layers=2, vocab=1000)
+    model = DecodeModel(cfg, context=256, seed=5)
+    model.token.fill_(123)
+    for k in (3, 6):
+        model.step(k)
+        torch.cuda.synchronize()
+        got = model.hbuf.float().view(-1)
+        want = _reference_hidden(torch, engine, model, k)
+        err = float((got - want).norm() / want.norm())
+        assert err < 2e-2, (k, err)
