@@ -597,7 +597,8 @@ def run_e2e_step(torch, plans, world, steps: int = 20):
     """The metric end to end from host memory through the public step API
     (plan.StepPlan over the same decode launches and weight copies): per step
     one pinned H2D copy of every activation, the 24 GEMV launches (graph
-    replay), one D2H copy of every output, one synchronisation."""
+    replay; the copies are nodes of the same graph), one D2H copy of every
+    output, one synchronisation."""
     from paper_2402_10517_b200 import plan as plan_mod
 
     sp = plan_mod.StepPlan([p for _, _, p in plans])
@@ -616,7 +617,7 @@ def run_e2e_step(torch, plans, world, steps: int = 20):
     return {"value": round(step_bytes() / world / dt / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": sp.h2d_bytes, "d2h_bytes_per_step": sp.d2h_bytes,
             "ms_per_step": round(dt * 1e3, 3),
-            "api": "plan.StepPlan.run_host(): pinned H2D of all x, 24 GEMV launches (graph), D2H of all y, sync"
+            "api": "plan.StepPlan.run_host(): one CUDA graph per step = pinned H2D of all x, 24 GEMV launches, D2H of all y; then sync"
                    + ("" if world == 1 else " (rank 0 shard only)")}
 
 

@@ -211,28 +211,39 @@ class StepPlan:
         self.h2d_bytes = n_x * 2
         self.d2h_bytes = ybytes
         self._graph = None
+        self._graph_copies = False
 
     def launch(self):
         for p in self.plans:
             p.run()
 
-    def capture(self):
-        """Record the launches into a CUDA graph (run ``launch()`` once first)."""
+    def capture(self, host_copies: bool = True):
+        """Record the step into a CUDA graph (run ``launch()`` once first).
+        host_copies: the pinned H2D copy of the inputs and the D2H copy of the
+        outputs are graph nodes too, so ``run_host()`` is one graph launch and
+        one synchronisation (the copies still run every step)."""
         torch = dev.require_cuda()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
+            if host_copies:
+                self._xd.copy_(self._xh, non_blocking=True)
             self.launch()
-        self._graph = g
+            if host_copies:
+                self._yh.copy_(self._yd, non_blocking=True)
+        self._graph, self._graph_copies = g, host_copies
         return g
 
     def run_host(self):
         """x_host -> device, the step's launches, device -> y_host; returns y_host."""
         torch = dev.require_cuda()
-        self._xd.copy_(self._xh, non_blocking=True)
-        if self._graph is not None:
+        if self._graph is not None and self._graph_copies:
             self._graph.replay()
         else:
-            self.launch()
-        self._yh.copy_(self._yd, non_blocking=True)
+            self._xd.copy_(self._xh, non_blocking=True)
+            if self._graph is not None:
+                self._graph.replay()
+            else:
+                self.launch()
+            self._yh.copy_(self._yd, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return self.y_host

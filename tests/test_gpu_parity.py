@@ -482,6 +482,18 @@ def test_step_plan_host_roundtrip(api):
     assert torch.equal(y[0][0], engine.gemv(preps[0], x0, cfg3))
     assert torch.equal(y[1][0], engine.gemv(preps[1], x0, cfg3))
     assert torch.equal(y[2][0], engine.gemv(preps[2], x1, cfg8))
+    # the copies are graph nodes: new host inputs are read on every replay, and
+    # the copy-less graph (host copies issued around it) gives the same bits
+    for x in sp.x_host:
+        x.copy_(torch.randn(x.shape, generator=g).half())
+    y2 = [t.clone() for t in sp.run_host()]
+    x0 = sp.x_host[0][0, :4096].clone()
+    x1 = sp.x_host[1][0, :3000].clone()
+    assert torch.equal(y2[0][0], engine.gemv(preps[0], x0, cfg3))
+    assert torch.equal(y2[2][0], engine.gemv(preps[2], x1, cfg8))
+    sp.capture(host_copies=False)
+    y3 = [t.clone() for t in sp.run_host()]
+    assert all(torch.equal(a, b) for a, b in zip(y2, y3))
 
 
 @pytest.mark.parametrize("shape", [(333, 1500), (17, 300), (1000, 11008), (4096, 3000)])
