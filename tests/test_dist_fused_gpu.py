@@ -187,3 +187,56 @@ def test_survey_named_entry_points_allgather_and_gemm_small():
         assert int(ctrl[r][2]) == 0
         assert torch.allclose(outs[r], ref.y[0], rtol=1e-5, atol=1e-5)
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.fixture(scope="module")
+def layers70b():
+    """BASELINE configs[3]: Llama-2-70B layer shapes (q/o 8192x8192, gate/up
+    28672x8192 sharing x; down 8192x28672), random codes / sorted tables."""
+    return {"qg": [_layer(70, 8192, 8192), _layer(71, 28672, 8192)], "down": [_layer(72, 8192, 28672)]}
+
+
+@pytest.mark.parametrize("world,k", [(2, 3), (4, 8), (8, 3), (8, 6)])
+def test_fused_allgather_llama70b_shapes(layers70b, world, k):
+    """configs[3] as a parity case: every 70B shape row-sharded over `world`
+    simulated ranks with the fused all-gather; every rank ends the step holding
+    the full output, bit-identical to the per-shard plain launches, and the
+    gathered numbers match the unsharded layer."""
+    import torch
+
+    from paper_2402_10517_b200 import dist, engine, plan
+
+    g = torch.Generator(device="cuda").manual_seed(700 + world * 10 + k)
+    for name, layers in layers70b.items():
+        cols = layers[0].shape[1]
+        full_rows = [L.shape[0] for L in layers]
+        _, nbytes = dist.output_layout(full_rows, 1, 2)
+        gathers = dist.PeerGather.simulated(nbytes, world)
+        shard_preps = [[engine.prepare(dist.shard_layer(L, world, r)) for L in layers] for r in range(world)]
+        plans = [dist.ShardedGemvPlan(shard_preps[r], full_rows, k, gathers[r], m=1, y_fp16=True,
+                                      shared_x=len(layers) > 1, spin_limit=1 << 22) for r in range(world)]
+        refs = [plan.GemvPlan(shard_preps[r], k, m=1, grouped=True, shared_x=len(layers) > 1, y_fp16=True)
+                for r in range(world)]
+        x = torch.randn(1, cols, device="cuda", generator=g).half()
+        for p in plans + refs:
+            for xb in {id(t): t for t in p.x}.values():
+                xb[:, :cols].copy_(x)
+        for p in plans:
+            p.launch_gemv()
+        for p in plans:
+            p.launch_wait()
+        for p in refs:
+            p.run()
+        torch.cuda.synchronize()
+        assert all(gathers[r].status() == 0 for r in range(world))
+        for i in range(len(layers)):
+            want = torch.cat([refs[r].y[i] for r in range(world)], dim=1)
+            for r in range(world):
+                assert torch.equal(plans[r].y[i], want), (name, r, i)
+        y_full = engine.gemv(engine.prepare(layers[-1]), x[0], engine.GemvConfig(bit_width=k, activations_fp16=True))
+        err = float((plans[world - 1].y[-1][0].float() - y_full.float()).norm() / y_full.float().norm())
+        assert err < 2e-3, (name, err)
+        for gt in gathers:
+            gt.close()
+        del plans, refs, shard_preps
+        torch.cuda.empty_cache()
