@@ -518,6 +518,25 @@ def test_tma_kernel_paths_vs_oracle(api, shape):
             assert err < TOL, (shape, k, m, fp16, err)
 
 
+@pytest.mark.parametrize("shape", [(11008, 4096), (4096, 11008)])
+def test_small_batch_llama7b_mlp_shapes_vs_oracle(api, shape):
+    # BASELINE configs[2]: the small-batch any-precision GEMM (M = 1, 2, 4, 8) on
+    # the Llama-2-7B MLP shapes at k = 3, 4, 8 (engine.py:312-341), vs the oracle
+    _, _, engine, _ = api
+    rows, cols = shape
+    layer = _random_layer(api, 11 + rows, rows, cols)
+    prep = engine.prepare(layer)
+    planes = prep.planes.cpu().numpy()
+    rng = np.random.default_rng(rows + 7 * cols)
+    for k in (3, 4, 8):
+        for m in (1, 2, 4, 8):
+            x = rng.standard_normal((m, cols))
+            y = engine.gemm(prep, x, engine.GemvConfig(bit_width=k, activations_fp16=True))
+            want = ora.gemm(planes, cols, k, layer.centroid_tables[k], ora.prep_x(x, cols, True), nthreads=8)
+            err = ora.rel_err(y, want)
+            assert err < TOL, (shape, k, m, err)
+
+
 @pytest.mark.parametrize("m,fp16", [(1, False), (1, True), (4, False)])
 def test_glu_epilogue_matches_silu_of_plain_outputs(api, m, fp16):
     """APB_FLAG_GLU: interleaved (gate, up) rows -> silu(gate . x) * (up . x) from
