@@ -681,7 +681,8 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                 mbar_wait(b_lfull + 8 * (jl & 1), (jl >> 1) & 1);
                 if (kCoopFirst && jl == 0) {
                     build(std::true_type{}, 0, WC, WC + 1);
-                    asm volatile("bar.sync 1, %0;" ::"r"((WC + 1) * 32) : "memory");  // with the compute warps
+                    __syncwarp();
+                    asm volatile("barrier.sync 1, %0;" ::"r"((WC + 1) * 32) : "memory");  // with the compute warps
                 } else {
                     build(std::false_type{}, jl & 1, 0, 1);
                 }
@@ -914,7 +915,8 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
         if (kCoopFirst && jl == 0) {  // first table: built by all compute warps + the service warp
             mbar_sleep(b_lfull, 0);
             build(std::true_type{}, 0, warp, WC + 1);
-            asm volatile("bar.sync 1, %0;" ::"r"((WC + 1) * 32) : "memory");
+            __syncwarp();
+            asm volatile("barrier.sync 1, %0;" ::"r"((WC + 1) * 32) : "memory");
         } else {
             mbar_sleep(b_tready + 8 * (jl & 1), (jl >> 1) & 1);  // table of this item
         }
