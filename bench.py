@@ -597,11 +597,12 @@ def run_e2e_step(torch, plans, world, steps: int = 20):
     """The metric end to end from host memory through the public step API
     (plan.StepPlan over the same decode launches and weight copies): per step
     one pinned H2D copy of every activation, the 24 GEMV launches (graph
-    replay; the copies are nodes of the same graph), one D2H copy of every
-    output, one synchronisation."""
+    replay; the copy is a node of the same graph), the outputs stored by the
+    GEMV epilogues straight into pinned host memory (zero_copy_y: the D2H bytes
+    cross PCIe as posted writes during the step), one synchronisation."""
     from paper_2402_10517_b200 import plan as plan_mod
 
-    sp = plan_mod.StepPlan([p for _, _, p in plans])
+    sp = plan_mod.StepPlan([p for _, _, p in plans], zero_copy_y=True)
     for x in sp.x_host:
         x.copy_(torch.randn(x.shape, dtype=torch.float32).half())
     sp.launch()
@@ -617,7 +618,8 @@ def run_e2e_step(torch, plans, world, steps: int = 20):
     return {"value": round(step_bytes() / world / dt / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": sp.h2d_bytes, "d2h_bytes_per_step": sp.d2h_bytes,
             "ms_per_step": round(dt * 1e3, 3),
-            "api": "plan.StepPlan.run_host(): one CUDA graph per step = pinned H2D of all x, 24 GEMV launches, D2H of all y; then sync"
+            "api": "plan.StepPlan(zero_copy_y=True).run_host(): one CUDA graph per step = pinned H2D of all x, "
+                   "24 GEMV launches whose epilogues store y into pinned host memory over PCIe; then sync"
                    + ("" if world == 1 else " (rank 0 shard only)")}
 
 

@@ -104,8 +104,12 @@ class GemvPlan:
         if len(x_list) != len(self.x) or len(y_list) != len(self.y):
             raise ParameterError("rebind needs one x and one y per layer")
         for old, new in list(zip(self.x, x_list)) + list(zip(self.y, y_list)):
-            if tuple(old.shape) != tuple(new.shape) or old.dtype != new.dtype or not new.is_cuda:
+            if tuple(old.shape) != tuple(new.shape) or old.dtype != new.dtype:
                 raise ParameterError("rebind buffers must match the plan's shapes and dtypes")
+        # x on the device; y on the device or in pinned host memory (UVA: the
+        # epilogue stores straight into it over PCIe, StepPlan zero_copy_y)
+        if not all(x.is_cuda for x in x_list) or not all(y.is_cuda or y.is_pinned() for y in y_list):
+            raise ParameterError("rebind: x must be device tensors, y device or pinned host tensors")
         self.x, self.y = list(x_list), list(y_list)
         self._xp = ptr_array([dev.ptr(x) for x in self.x])
         self._yp = ptr_array([dev.ptr(y) for y in self.y])
@@ -172,9 +176,14 @@ class StepPlan:
     graph after ``capture()``), one D2H copy of every output, one stream
     synchronisation.  ``x_host`` / ``y_host`` are the pinned views the caller
     fills / reads (one per distinct activation / per output, in plan order).
+
+    zero_copy_y: the GEMV epilogues store the outputs straight into the pinned
+    host block (a pinned allocation is device-addressable under UVA), so the
+    D2H copy disappears from the end of the step; the same bytes cross PCIe
+    as posted writes overlapped with the remaining launches.
     """
 
-    def __init__(self, plans):
+    def __init__(self, plans, zero_copy_y: bool = False):
         torch = dev.require_cuda()
         self.plans = list(plans)
         xs, seen = [], {}
@@ -203,6 +212,9 @@ class StepPlan:
             yviews.append(self._yd[off:off + nb].view(y.dtype).view(y.shape))
             yhost.append(self._yh[off:off + nb].view(y.dtype).view(y.shape))
             off += nb
+        self.zero_copy_y = zero_copy_y
+        if zero_copy_y:
+            yviews = yhost
         yi = 0
         for p in self.plans:
             p.rebind([xviews[seen[x.data_ptr()]] for x in p.x], yviews[yi:yi + len(p.y)])
@@ -228,7 +240,7 @@ class StepPlan:
             if host_copies:
                 self._xd.copy_(self._xh, non_blocking=True)
             self.launch()
-            if host_copies:
+            if host_copies and not self.zero_copy_y:
                 self._yh.copy_(self._yd, non_blocking=True)
         self._graph, self._graph_copies = g, host_copies
         return g
@@ -244,6 +256,7 @@ class StepPlan:
                 self._graph.replay()
             else:
                 self.launch()
-            self._yh.copy_(self._yd, non_blocking=True)
+            if not self.zero_copy_y:
+                self._yh.copy_(self._yd, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return self.y_host

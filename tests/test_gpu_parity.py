@@ -494,6 +494,18 @@ def test_step_plan_host_roundtrip(api):
     sp.capture(host_copies=False)
     y3 = [t.clone() for t in sp.run_host()]
     assert all(torch.equal(a, b) for a, b in zip(y2, y3))
+    # zero-copy outputs: the epilogues store into the pinned host block itself
+    zp = [plan.GemvPlan(preps[:2], 3, grouped=True, pdl=True, shared_x=True),
+          plan.GemvPlan([preps[2]], 8, grouped=False, pdl=True)]
+    sz = plan.StepPlan(zp, zero_copy_y=True)
+    for a, b in zip(sz.x_host, sp.x_host):
+        a.copy_(b)
+    sz.launch()
+    torch.cuda.synchronize()
+    sz.capture()
+    for _ in range(3):
+        y4 = [t.clone() for t in sz.run_host()]
+    assert all(torch.equal(a, b) for a, b in zip(y2, y4))
 
 
 @pytest.mark.parametrize("shape", [(333, 1500), (17, 300), (1000, 11008), (4096, 3000)])
