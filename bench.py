@@ -11,11 +11,16 @@ dependent launch and replayed from a CUDA graph.
 
 value: whole-job algorithmic HBM GB/s = sum of SURVEY.md section 8(d) bytes
 (R*C*k/8 + R*2^k*2 + C*2 + R*2 per GEMV) / device time (CUDA events on the
-launch stream, max over ranks).  Inputs are resident in HBM; the weights are
-rotated over 4 copies (4 x 203 MB) per launch, so no launch finds its planes in
-the 126 MB L2.  With N > 1 GPUs every layer is row-sharded (rank i holds rows
-[i*R/N, (i+1)*R/N)) and each GEMV is followed by an NCCL all-gather of the
-output slices (strong scaling: total work fixed).
+launch stream, max over ranks).  Inputs are resident in HBM and larger than
+L2 by construction: 4 full copies of the layer set (4 x 203 MB), and launch
+(k_i, group g) reads copy (g + k_i) mod 4, so a layer's planes are re-read only
+4 bit-widths later with >= 3 whole bit-width sets (> 300 MB, > 2x the 126 MB
+L2) read in between; every detail leg rotates over > 2x L2 of distinct bytes.
+With N > 1 GPUs every layer is row-sharded (rank i holds rows
+[i*R/N, (i+1)*R/N)) and each GEMV's output slices are all-gathered (fused into
+the GEMV epilogue over NVLink P2P, or NCCL) -- strong scaling: total work
+fixed.  `--gpus N` without a launcher re-executes itself under
+torch.distributed.run with N ranks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -149,19 +154,55 @@ def make_layer_set(torch, seed: int, rank: int = 0, world: int = 1):
     return preps
 
 
+def copy_index(ki: int, gi: int) -> int:
+    """Weight copy read by launch group gi at bit-width index ki: group g cycles
+    through the copies as k grows, so the same planes come back only 4
+    bit-widths later (>= 3 full bit-width sets, > 300 MB, read in between)."""
+    return (gi + ki) % N_COPIES
+
+
 def decode_plans(plan_mod, copies, pdl: bool):
-    """Per k: grouped q/k/v, o, grouped gate/up, down; weight copy rotated per launch.
-    fp16 outputs (the metric's byte count, has M*R*2 output bytes)."""
-    plans, i = [], 0
-    for k in BITS:
-        for grp in GROUPS:
-            c = copies[i % len(copies)]
+    """Per k: grouped q/k/v, o, grouped gate/up, down; the weight copy of each
+    launch from copy_index (L2-clean).  fp16 outputs (the metric's byte count,
+    SURVEY 8(d), has M*R*2 output bytes)."""
+    plans = []
+    for ki, k in enumerate(BITS):
+        for gi, grp in enumerate(GROUPS):
+            c = copies[copy_index(ki, gi)]
             p = plan_mod.GemvPlan([c[j] for j in grp], k, m=1, grouped=True, pdl=pdl,
                                   shared_x=len(grp) > 1, y_fp16=True)
             p.x[0].normal_()
             plans.append((k, grp, p))
-            i += 1
     return plans
+
+
+def l2_bytes(torch) -> int:
+    try:
+        return int(torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size)
+    except Exception:
+        return 126 * 1024 * 1024
+
+
+def clone_prep(prep):
+    """A prepared layer with its own copy of the bitplanes (tables shared):
+    distinct HBM bytes for L2-clean rotation."""
+    import copy as _copy
+    from dataclasses import replace
+
+    c = _copy.copy(prep)
+    c.tensor = replace(prep.tensor, planes=prep.tensor.planes.clone())
+    return c
+
+
+def rotation_pool(torch, preps, bytes_per_launch: int):
+    """preps extended with plane clones until one pass over the pool reads more
+    than 2x L2 of distinct bytes (the rotation then never hits L2)."""
+    need = 2 * l2_bytes(torch) + 1
+    n = max(len(preps), -(-need // max(1, bytes_per_launch)))
+    pool = list(preps)
+    while len(pool) < n:
+        pool.append(clone_prep(preps[len(pool) % len(preps)]))
+    return pool
 
 
 def fused_plans(torch, copies):
@@ -181,9 +222,7 @@ def fused_plans(torch, copies):
             gathers.append(pdist.PeerGather(nbytes))
             specs.append((k, grp, copies[i % len(copies)], full_rows))
             i += 1
-    bad = torch.tensor([0 if all(g.ok for g in gathers) else 1], device="cuda", dtype=torch.int32)
-    dist.all_reduce(bad, op=dist.ReduceOp.MAX)
-    if int(bad.item()):
+    if _allreduce_max(torch, 0 if all(g.ok for g in gathers) else 1):
         for g in gathers:
             g.close()
         return None
@@ -244,14 +283,21 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2402_10517_b200 import plan
-    from paper_2402_10517_b200.dist import gather_rows
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # APB_BENCH_SHARE_GPU=1 (debug): every rank on cuda:0 over gloo, to exercise
+    # the N > 1 code path (fused gather through CUDA IPC) on a one-GPU box
+    share = os.environ.get("APB_BENCH_SHARE_GPU") == "1" and world > 1
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peak, peak_kind = peaks()
 
     copies = [make_layer_set(torch, 1234 + c, rank, world) for c in range(N_COPIES)]
@@ -262,7 +308,7 @@ def run_ours(args):
     fused, gather_mode = None, "none (1 GPU)"
     if world > 1:
         gather_mode = "nccl all_gather_into_tensor after each GEMV"
-        if not args.nccl_gather:
+        if not args.nccl_gather or share:
             fused = fused_plans(torch, copies)  # collective on every rank; None if any rank lacks P2P / IPC
             if fused is None:
                 print("[bench] fused gather unavailable (CUDA IPC / P2P); using NCCL", file=sys.stderr)
@@ -278,7 +324,7 @@ def run_ours(args):
             p.run()
             if world > 1:
                 for j, li in enumerate(grp):
-                    gather_rows(p.y[j], SHAPES[li][1])
+                    _gather(torch, p.y[j], SHAPES[li][1], share)
 
     if fused is not None:  # self-check: one aligned step, short waits, every rank saw every arrival
         for sp in fused:
@@ -286,19 +332,17 @@ def run_ours(args):
         dist.barrier()
         step()
         torch.cuda.synchronize()
-        bad = torch.tensor([max(sp.gather.status() for sp in fused)], device="cuda", dtype=torch.int32)
-        dist.all_reduce(bad, op=dist.ReduceOp.MAX)
-        if not int(bad.item()):  # and the gathered numbers: the first launch vs plain GEMV + NCCL
+        bad = _allreduce_max(torch, max(sp.gather.status() for sp in fused))
+        if not bad:  # and the gathered numbers: the first launch vs plain GEMV + gathered slices
             sp, (_, grp, p) = fused[0], plans[0]
             p.x[0].copy_(sp.x[0])
             p.run()
             sp.run()
             torch.cuda.synchronize()
-            same = all(torch.equal(sp.y[j], gather_rows(p.y[j], SHAPES[li][1]).to(sp.y[j].dtype))
+            same = all(torch.equal(sp.y[j], _gather(torch, p.y[j], SHAPES[li][1], share).to(sp.y[j].dtype))
                        for j, li in enumerate(grp))
-            bad.fill_(0 if same else 1)
-            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
-        if int(bad.item()):
+            bad = _allreduce_max(torch, 0 if same else 1)
+        if bad:
             print("[bench] fused gather self-check failed; using NCCL", file=sys.stderr)
             fused, gather_mode = None, "nccl all_gather_into_tensor after each GEMV (fused self-check failed)"
         else:
@@ -339,9 +383,7 @@ def run_ours(args):
         dist.barrier()
     ms = start.elapsed_time(end)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _allreduce_max(torch, ms)
     clocks = clk.summary()
     ms_per_step = ms / args.steps
     value = step_bytes() / (ms_per_step * 1e-3) / 1e9
@@ -359,7 +401,10 @@ def run_ours(args):
                    "shapes": [f"{n}:{r}x{c}" for n, r, c in SHAPES], "bits": BITS, "batch": 1,
                    "n_max": N_MAX, "launch_groups": "qkv | o | gate+up | down per k (PDL chain)",
                    "launches_per_step": len(plans), "cuda_graph": graph is not None,
-                   "l2": f"inputs > L2: weights rotated over {N_COPIES} copies (4 x 203 MB) per launch"},
+                   "l2": (f"inputs > L2 by construction: {N_COPIES} copies of the layer set "
+                          f"({N_COPIES} x 203 MB), launch (k_i, group g) reads copy (g + k_i) mod {N_COPIES}: "
+                          "a layer's planes return only 4 bit-widths later, after >= 3 full bit-width "
+                          "sets (> 300 MB > 2x L2); planes loaded L2::evict_first")},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": round(value, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(value / peak, 4), "peak_kind": peak_kind,
@@ -376,10 +421,17 @@ def run_ours(args):
             print(json.dumps(result))
         return
     if world == 1:
-        result["per_gemv_us"] = per_gemv_detail(torch, plan, copies)
+        result["per_gemv_us"] = per_gemv_detail(torch, plan, copies, peak)
+        result["fp16_cublas_gemv"] = fp16_gemv_detail(torch, result["per_gemv_us"])
         result["grouped_all7_GBps"] = grouped_all7(torch, plan, copies)
+        result["packer"] = packer_detail(torch)
         result["small_batch_C3"] = small_batch_detail(torch, plan, copies)
         result["shard70b_C4_per_rank"] = shard70b_detail(torch, plan)
+    if world > 1:
+        try:
+            result["shard70b_C4"] = shard70b_multi(torch, plan, world, rank, share)
+        except Exception as e:  # never lose the headline to the side leg
+            result["shard70b_C4"] = {"error": f"{type(e).__name__}: {e}"[:300]}
         if not args.no_decode:
             result["decode_step"] = run_decode(torch)
             result["quantizer"] = run_quantizer(torch)
@@ -397,12 +449,152 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _allreduce_max(torch, v: float) -> float:
+    """MAX over ranks of a host scalar (device tensor on NCCL, host on gloo)."""
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        return v
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([float(v)], device="cuda" if on_dev else "cpu", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _gather(torch, y, rows: int, share: bool):
+    """All-gather of row slices: NCCL, or via host tensors on the gloo debug path."""
+    from paper_2402_10517_b200.dist import gather_rows
+
+    if not share:
+        return gather_rows(y, rows)
+    import torch.distributed as dist
+
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, y.cpu())
+    return torch.cat(parts, dim=-1).to(y.device)
+
+
+def shard70b_multi(torch, plan, world: int, rank: int, share: bool):
+    """BASELINE configs[3] at N > 1: the Llama-2-70B shapes row-sharded over the
+    ranks (k = 3, 4, 8), each launch L2-clean (rotation pool).  Per shape and k:
+    the per-rank GEMV alone, the GEMV with the all-gather fused into its
+    epilogue (P2P stores over NVLink + arrival counters + wait kernel), and the
+    GEMV followed by an NCCL all-gather; µs per layer, max over ranks."""
+    import torch.distributed as dist
+
+    from paper_2402_10517_b200 import AnyPrecisionLayer, engine
+    from paper_2402_10517_b200 import dist as pdist
+
+    shapes = [("8192x8192", 8192, 8192), ("28672x8192", 28672, 8192), ("8192x28672", 8192, 28672)]
+    out = {"world": world, "note": "us per layer (max over ranks); fused = GEMV epilogue stores into every "
+                                   "rank's IPC-mapped output + pdist wait kernel; nccl = GEMV + all_gather"}
+    g = torch.Generator(device="cuda").manual_seed(70 + rank)
+
+    def timed(fn, n):
+        fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(3):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return _allreduce_max(torch, a.elapsed_time(b) * 1e3 / (3 * n))
+
+    for name, rows, cols in shapes:
+        r0, r1 = pdist.shard_bounds(rows, world, rank)
+        codes = torch.randint(0, 256, (r1 - r0, cols), dtype=torch.uint8, device="cuda", generator=g)
+        tables = {k: torch.sort(torch.randn(r1 - r0, 1 << k, device="cuda", generator=g), 1).values.half()
+                  for k in range(3, 9)}
+        base = engine.prepare(AnyPrecisionLayer(n_min=3, n_max=8, codes=codes, centroid_tables=tables,
+                                                shape=(r1 - r0, cols)))
+        del codes
+        for k in (3, 4, 8):
+            pool = rotation_pool(torch, [base], (r1 - r0) * cols * k // 8)
+            ps = [plan.GemvPlan([p], k, grouped=True, pdl=True, y_fp16=True) for p in pool]
+            for p in ps:
+                p.x[0].normal_()
+            d = {"rank_rows": r1 - r0}
+            d["gemv_us"] = round(timed(lambda: [p.run() for p in ps], len(ps)), 2)
+            _, nbytes = pdist.output_layout([rows], 1, 2)
+            gathers = [pdist.PeerGather(nbytes) for _ in pool]
+            if _allreduce_max(torch, 0 if all(gt.ok for gt in gathers) else 1) == 0:
+                sps = [pdist.ShardedGemvPlan([p], [rows], k, gt, m=1, y_fp16=True) for p, gt in zip(pool, gathers)]
+                d["fused_us"] = round(timed(lambda: [sp.run() for sp in sps], len(sps)), 2)
+                d["fused_status"] = int(_allreduce_max(torch, max(sp.gather.status() for sp in sps)))
+                del sps
+            for gt in gathers:
+                gt.close()
+            if not share:
+                d["nccl_us"] = round(timed(lambda: [(p.run(), _gather(torch, p.y[0], rows, False)) for p in ps],
+                                           len(ps)), 2)
+            out.setdefault(name, {})[f"k{k}"] = d
+            del ps, pool
+        del base
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank launch plumbing only (no GPU): every rank joins a
+    gloo group, all-reduces its rank, rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    total = rank
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([rank], dtype=torch.int64)
+        dist.all_reduce(t)
+        total = int(t.item())
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "rank_sum": total, "gpus_arg": args.gpus}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(args, argv):
+    """--gpus N > 1 with no launcher around us: re-execute under
+    torch.distributed.run (one rank per GPU, rendezvous on 127.0.0.1).  Returns
+    the child's exit status, or None when this process is already a rank (or
+    N == 1).  Refuses loudly when the box has fewer GPUs than asked for."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != args.gpus:
+            raise SystemExit(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}")
+        return None
+    if args.gpus <= 1:
+        return None
+    if not args.dry_run and args.impl == "ours" and os.environ.get("APB_BENCH_SHARE_GPU") != "1":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible; refusing",
+                  file=sys.stderr)
+            return 3
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
+
+
 def run_decode(torch, steps: int = 20):
     """BASELINE config C5: full random-init Llama-2-7B single-token decode step
     (32 blocks, every linear through the bitplane GEMV at bit-width k, torch glue,
-    one CUDA graph per k, context 1024) -> tokens/s; plus GPU packer throughput
-    (pack_bitplanes + permute_layout of an 11008x4096 code matrix, 8 planes)."""
-    from paper_2402_10517_b200 import bitplane
+    one CUDA graph per k, context 1024) -> tokens/s (the packer leg is
+    packer_detail)."""
     from paper_2402_10517_b200.decode import DecodeModel
 
     model = DecodeModel(context=1024)
@@ -425,21 +617,6 @@ def run_decode(torch, steps: int = 20):
                                  "quantized_GBps": round(model.quantized_bytes(k) / (ms * 1e-3) / 1e9, 1)}
     del model
     torch.cuda.empty_cache()
-    # packer
-    g = torch.Generator(device="cuda").manual_seed(7)
-    codes = torch.randint(0, 256, (11008, 4096), dtype=torch.uint8, device="cuda", generator=g)
-    t = bitplane.pack_bitplanes(codes, 8)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(20):
-        t = bitplane.pack_bitplanes(codes, 8)
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / 20
-    nbytes = codes.numel() + t.planes.numel()
-    out["packer"] = {"shape": "11008x4096 codes -> 8 bitplanes (linear layout)", "ms": round(ms, 4),
-                     "GBps": round(nbytes / (ms * 1e-3) / 1e9, 1)}
     return out
 
 
@@ -500,19 +677,21 @@ def run_quantizer(torch):
 
 
 def _chain_us(torch, plan, preps_copies, k, m, reps=10):
-    """µs per launch of a PDL chain of 5 x len(copies) launches (rotating copies)."""
-    ps = [plan.GemvPlan([c], k, m=m, grouped=False, pdl=True) for c in preps_copies]
+    """µs per launch of a PDL chain over a rotation pool of the layer (> 2x L2
+    of distinct plane bytes per pass: no launch finds its planes in L2)."""
+    p0 = preps_copies[0]
+    pool = rotation_pool(torch, preps_copies, p0.tensor.rows * p0.tensor.cols * k // 8)
+    ps = [plan.GemvPlan([c], k, m=m, grouped=False, pdl=True) for c in pool]
     for p in ps:
         for x in p.x:
             x.normal_()
 
     def chain():
-        for _ in range(5):
-            for p in ps:
-                p.run()
+        for p in ps:
+            p.run()
 
     _, ms = time_graph(torch, chain, reps)
-    return ms * 1e3 / (5 * len(ps))
+    return ms * 1e3 / len(ps)
 
 
 def small_batch_detail(torch, plan, copies):
@@ -546,7 +725,7 @@ def shard70b_detail(torch, plan):
         for P in (1, 2, 4, 8):
             r = rows // P
             copies = []
-            for _ in range(2):
+            for _ in range(1):  # plane clones of this copy make the L2-clean rotation pool
                 codes = torch.randint(0, 256, (r, cols), dtype=torch.uint8, device="cuda", generator=g)
                 tables = {k: torch.sort(torch.randn(r, 1 << k, device="cuda", generator=g), 1).values.half()
                           for k in range(3, 9)}
@@ -562,28 +741,87 @@ def shard70b_detail(torch, plan):
     return out
 
 
-def per_gemv_detail(torch, plan, copies):
-    """Each GEMV alone: a PDL chain of 4 x 5 identical launches (rotating
-    copies) in a graph; µs per launch and GB/s."""
+def per_gemv_detail(torch, plan, copies, peak):
+    """configs[0..1] per shape x k, L2-clean: each distinct GEMV shape alone in
+    a PDL chain over a rotation pool (> 2x L2 of distinct planes per pass);
+    µs per launch, algorithmic GB/s and the fraction of the measured peak."""
     out = {}
     for k in BITS:
-        for li, (n, r, c) in enumerate(SHAPES):
-            ps = [plan.GemvPlan([copies[j][li]], k, grouped=False, pdl=True) for j in range(N_COPIES)]
+        for li, (n, r, c) in ((3, SHAPES[3]), (4, SHAPES[4]), (6, SHAPES[6])):
+            us = _chain_us(torch, plan, [cp[li] for cp in copies], k, 1)
+            gbps = alg_bytes(r, c, k) / (us * 1e-6) / 1e9
+            out.setdefault(f"k{k}", {})[f"{r}x{c}"] = {
+                "us": round(us, 2), "GBps": round(gbps, 1), "frac_of_peak": round(gbps / peak, 3)}
+    return out
 
-            def chain():
-                for _ in range(5):
-                    for p in ps:
-                        p.run()
 
-            _, ms = time_graph(torch, chain, 10)
-            us = ms * 1e3 / (5 * len(ps))
-            out.setdefault(f"k{k}", {})[f"{n}_{r}x{c}"] = {
-                "us": round(us, 2), "GBps": round(alg_bytes(r, c, k) / (us * 1e-6) / 1e9, 1)}
+def fp16_gemv_detail(torch, per_gemv):
+    """The paper's comparator: a dense fp16 GEMV
+    through cuBLAS (torch.mv, fp16 weights) on the same shapes, L2-clean (a
+    rotation pool of weight copies > 2x L2), and the bitplane kernel's speedup
+    over it per k (context, not a target)."""
+    out = {}
+    for r, c in ((4096, 4096), (11008, 4096), (4096, 11008)):
+        nbytes = r * c * 2
+        n = max(2, -(-(2 * l2_bytes(torch) + 1) // nbytes))
+        ws = [torch.randn(r, c, device="cuda").half() for _ in range(n)]
+        x = torch.randn(c, device="cuda").half()
+        ys = [torch.empty(r, device="cuda", dtype=torch.float16) for _ in range(n)]
+
+        def chain():
+            for w, y in zip(ws, ys):
+                torch.mv(w, x, out=y)
+
+        _, ms = time_graph(torch, chain, 10)
+        us = ms * 1e3 / n
+        d = {"us": round(us, 2), "GBps": round((nbytes + c * 2 + r * 2) / (us * 1e-6) / 1e9, 1),
+             "bitplane_speedup": {}}
+        for k in BITS:
+            bp = per_gemv.get(f"k{k}", {}).get(f"{r}x{c}")
+            if bp:
+                d["bitplane_speedup"][f"k{k}"] = round(us / bp["us"], 2)
+        out[f"{r}x{c}"] = d
+        del ws, ys
+    torch.cuda.empty_cache()
+    return out
+
+
+def packer_detail(torch):
+    """GPU packer (bitplane.pack_permuted: pack_bitplanes + permute_layout in
+    one pass, what engine.prepare runs), L2-clean: the apb_pack kernel over a
+    rotation of code matrices whose inputs + outputs exceed 2x L2; bytes =
+    R*C codes in + n_max*R*Cp/8 planes out."""
+    from paper_2402_10517_b200 import _device as dev
+    from paper_2402_10517_b200._lib import check, load
+
+    lib = load()
+    out = {}
+    for r, c in ((11008, 4096), (28672, 8192)):
+        per = r * c * 2  # codes in + 8 planes out (Cp == C for these shapes)
+        n = max(2, -(-(2 * l2_bytes(torch) + 1) // per))
+        g = torch.Generator(device="cuda").manual_seed(7)
+        codes = [torch.randint(0, 256, (r, c), dtype=torch.uint8, device="cuda", generator=g) for _ in range(n)]
+        planes = [torch.empty((8, r, c // 8), dtype=torch.uint8, device="cuda") for _ in range(n)]
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+        def chain():
+            for cd, pl in zip(codes, planes):
+                check(lib.apb_pack(dev.ptr(cd), r, c, c, 8, 1, dev.ptr(pl), dev.ptr(flag), dev.stream_ptr()),
+                      "apb_pack")
+
+        _, ms = time_graph(torch, chain, 5)
+        us = ms * 1e3 / n
+        out[f"{r}x{c}"] = {"us": round(us, 2), "GBps": round(per / (us * 1e-6) / 1e9, 1),
+                           "layout": "permuted (pack_permuted / prepare)", "rotation": n}
+        del codes, planes
+    torch.cuda.empty_cache()
     return out
 
 
 def grouped_all7(torch, plan, copies):
     ps = [plan.GemvPlan(copies[j % N_COPIES], k, grouped=True, pdl=True) for j, k in enumerate(BITS)]
+    # (6 launches over 4 copies: k and k+4 share a copy with the k+1..k+3 sets,
+    # > 300 MB, read in between)
 
     def step():
         for p in ps:
@@ -739,8 +977,14 @@ def main():
     ap.add_argument("--no-decode", action="store_true", help="skip the C5 decode-step leg")
     ap.add_argument("--nccl-gather", action="store_true",
                     help="N > 1: all-gather with NCCL after each GEMV instead of the fused epilogue stores")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only (gloo, no GPU work)")
     args = ap.parse_args()
-    if args.impl == "reference":
+    rc = launch_ranks(args, sys.argv[1:])
+    if rc is not None:
+        sys.exit(rc)
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -104,7 +104,11 @@ int apb_transpose_words(const uint32_t* plane_words, int k, int64_t n, uint32_t*
  * (uint16 fp16 [rows][1<<k]).
  *   x      : fp16 [m_x][ldx] activations.  With x_split = 1 the m_x rows are
  *            (hi, lo) pairs of an fp32 activation (x = hi + lo) and the output
- *            has m_x/2 rows: y[m] = W.(x_hi[m]) + W.(x_lo[m]).
+ *            has m_x/2 rows: y[m] = W.(x_hi[m]) + W.(x_lo[m]).  x_split = 2
+ *            ("scaled pairs", apb_split_x_scaled): the pairs hold x * s_m with
+ *            s_m a power of two, and m_x/2 floats 1/s_m follow the rows in the
+ *            same buffer (element offset m_x * ldx): y[m] = (W.hi + W.lo) / s_m,
+ *            so fp32 activations of any magnitude keep ~22 significant bits.
  *   y      : [m_out][ldy] of y_dtype (APB_DTYPE_F32 or APB_DTYPE_F16).
  * Accumulation is fp32 in a fixed order; results are bit-reproducible for
  * identical inputs and independent of planes k..n_max-1 (test_engine.py:165-176). */
@@ -161,6 +165,13 @@ int apb_split_hilo(const float* x, int64_t m, int64_t cols, int64_t ldx, uint16_
  * m rows fp16(x[i]) only (activations_fp16, engine.py:276-277). */
 int apb_split_x(const float* x, int m, int64_t cols, int64_t ldx_in, uint16_t* out,
                 int64_t ldx_out, int round_only, void* stream);
+
+/* x_split = 2 operand (engine.py:270-281 for fp32 activations): out [2m][ldx_out]
+ * = (hi, lo) pairs of x * s_r (s_r: the power of two putting row r's max |x| in
+ * [2^14, 2^15); hi = fp16(x*s_r), lo = fp16(x*s_r - hi), columns >= cols zero),
+ * followed by m floats 1/s_r at element offset 2m * ldx_out (ldx_out even). */
+int apb_split_x_scaled(const float* x, int m, int64_t cols, int64_t ldx_in, uint16_t* out,
+                       int64_t ldx_out, void* stream);
 
 /* Fused glue of a decoder block around the GEMVs (decode-step measurement,
  * BASELINE config C5; outside the reference's hot path).  Device pointers,

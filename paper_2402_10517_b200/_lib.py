@@ -65,6 +65,7 @@ SIGNATURES = {
     ),
     "apb_dequant": ([_P, _I, _I64, _I64, _I64, _I, _I, _P, _P, _I, _I64, _P], _I),
     "apb_split_x": ([_P, _I, _I64, _I64, _P, _I64, _I, _P], _I),
+    "apb_split_x_scaled": ([_P, _I, _I64, _I64, _P, _I64, _P], _I),
     "apb_rms_residual": ([_P, _P, _P, _P, _I64, ctypes.c_float, _P], _I),
     "apb_rope_cache": ([_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I64, _P], _I),
     "apb_silu_mul": ([_P, _P, _P, _I64, _P], _I),

@@ -24,9 +24,27 @@
 #pragma once
 
 #include <cuda_fp16.h>
+#include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace apb {
+
+// Host side: the dynamic shared-memory opt-in is a per-DEVICE function
+// attribute; one flag bit per device (a process may drive several GPUs).
+#include <atomic>
+#include <cuda_runtime.h>
+template <typename Kern>
+static inline bool ensure_smem_optin(Kern kern, int bytes, std::atomic<unsigned long long>& done) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    const unsigned long long bit = dev < 64 ? (1ull << dev) : 0ull;
+    if (bit && (done.load(std::memory_order_acquire) & bit)) return true;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+    if (bit) done.fetch_or(bit, std::memory_order_release);
+    return true;
+}
 
 constexpr int kTileWeights = 1024;
 constexpr int kTileBytes = 128;

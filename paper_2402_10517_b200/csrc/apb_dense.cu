@@ -16,6 +16,10 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// PAIRS = false: hi rows [0, m), lo rows [m, 2m) (dense GEMM operand).
+// PAIRS = true : rows (2r, 2r+1) = (hi, lo), columns cols..ld-1 zeroed (the
+//                quantized GEMV's x_split = 2 operand, see apb_split_x_scaled).
+template <bool PAIRS>
 __global__ void __launch_bounds__(kThreads) split_hilo_kernel(const float* __restrict__ x, int cols, int64_t ldx,
                                                               __half* __restrict__ out, int64_t ld, int m,
                                                               float* __restrict__ inv_scale) {
@@ -38,10 +42,10 @@ __global__ void __launch_bounds__(kThreads) split_hilo_kernel(const float* __res
         const int se = min(max(15 - e, -126), 126);
         scale = ldexpf(1.f, se);                // a * scale in [2^14, 2^15)
     }
-    __half* hi = out + (int64_t)row * ld;
-    __half* lo = out + (int64_t)(m + row) * ld;
-    for (int i = t; i < cols; i += kThreads) {
-        const float v = xr[i] * scale;          // exact (power of two)
+    __half* hi = out + (int64_t)(PAIRS ? 2 * row : row) * ld;
+    __half* lo = out + (int64_t)(PAIRS ? 2 * row + 1 : m + row) * ld;
+    for (int i = t; i < (PAIRS ? (int)ld : cols); i += kThreads) {
+        const float v = i < cols ? xr[i] * scale : 0.f;  // exact (power of two)
         const __half h = __float2half_rn(v);
         hi[i] = h;
         lo[i] = __float2half_rn(v - __half2float(h));
@@ -55,7 +59,21 @@ extern "C" int apb_split_hilo(const float* x, int64_t m, int64_t cols, int64_t l
                               float* inv_scale, void* stream) {
     if (!x || !out || !inv_scale) return APB_ERR_PARAM;
     if (m <= 0 || cols <= 0 || m > INT32_MAX || cols > INT32_MAX || ldx < cols || ld < cols) return APB_ERR_SHAPE;
-    split_hilo_kernel<<<(unsigned)m, kThreads, 0, (cudaStream_t)stream>>>(x, (int)cols, ldx, (__half*)out, ld,
-                                                                          (int)m, inv_scale);
+    split_hilo_kernel<false><<<(unsigned)m, kThreads, 0, (cudaStream_t)stream>>>(x, (int)cols, ldx, (__half*)out,
+                                                                                 ld, (int)m, inv_scale);
+    return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
+}
+
+// Quantized-path operand of x_split = 2 (engine.py:270-281 _prep_x for fp32
+// activations at fp32 accuracy): out [2m][ldx_out] (hi, lo) row pairs of x * s_r,
+// then m float inverse scales 1 / s_r at element offset 2m * ldx_out.
+extern "C" int apb_split_x_scaled(const float* x, int m, int64_t cols, int64_t ldx_in, uint16_t* out,
+                                  int64_t ldx_out, void* stream) {
+    if (!x || !out) return APB_ERR_PARAM;
+    if (m <= 0 || cols <= 0 || cols > INT32_MAX || ldx_in < cols || ldx_out < cols || (ldx_out & 1))
+        return APB_ERR_SHAPE;
+    float* inv = reinterpret_cast<float*>(out + (int64_t)2 * m * ldx_out);
+    split_hilo_kernel<true><<<(unsigned)m, kThreads, 0, (cudaStream_t)stream>>>(x, (int)cols, ldx_in, (__half*)out,
+                                                                                ldx_out, m, inv);
     return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
 }

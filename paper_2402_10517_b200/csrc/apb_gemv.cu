@@ -74,6 +74,7 @@ struct GemvProblem {
     int n_tiles;
     int item_begin;         // first global item (row block) of this problem
     int64_t cost_begin;     // prefix cost (tiles) of the items before this problem
+    const float* xinv;      // x_split == 2: per output row inverse activation scale (else null)
 };
 
 struct GemvLaunch {
@@ -415,6 +416,7 @@ __device__ __forceinline__ void service_role(const GemvLaunch& L, int first, int
 #pragma unroll
                     for (int w = 0; w < WC; ++w) lo += r[(w * kRowsPerCta + rl) * RC + 2 * m + 1];
                     sum = hi + lo;
+                    if (L.x_split == 2) sum *= P.xinv[m];  // scaled pairs: undo the power-of-two scale
                 } else {
                     sum = 0.f;
 #pragma unroll
@@ -952,13 +954,11 @@ template <int K, int NG, int UB, bool XS>
 static int launch_variant(const GemvLaunch& L, cudaStream_t s) {
     using LY = WsLayout<K, NG>;
     auto kern = gemv_kernel<K, NG, UB, XS>;
-    static std::atomic<int> configured{0};
-    if (!configured.load(std::memory_order_acquire)) {
+    static std::atomic<unsigned long long> configured{0};
+    {
         size_t max_smem = LY::total(XS ? kMaxXsBytes : 0);
         if (max_smem > kSmemLimitBytes) max_smem = kSmemLimitBytes;
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem) != cudaSuccess)
-            return APB_ERR_CUDA;
-        configured.store(1, std::memory_order_release);
+        if (!apb::ensure_smem_optin(kern, (int)max_smem, configured)) return APB_ERR_CUDA;
     }
     const size_t smem = LY::total(XS ? L.xs_bytes : 0);
     if (smem > kSmemLimitBytes) return APB_ERR_PARAM;
@@ -989,12 +989,8 @@ template <int K, int UB>
 static int launch6(const GemvLaunch& L, cudaStream_t s) {
     using G = G6<K, UB>;
     auto kern = gemv6_kernel<K, UB>;
-    static std::atomic<int> configured{0};
-    if (!configured.load(std::memory_order_acquire)) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimitBytes) != cudaSuccess)
-            return APB_ERR_CUDA;
-        configured.store(1, std::memory_order_release);
-    }
+    static std::atomic<unsigned long long> configured{0};
+    if (!apb::ensure_smem_optin(kern, (int)kSmemLimitBytes, configured)) return APB_ERR_CUDA;
     const size_t smem = G::total(L.xs_bytes);
     int grid = sm_count();
     if (grid > L.n_items) grid = L.n_items;
@@ -1058,7 +1054,7 @@ static int gemv_launch_chunk(int n, const uint8_t* const* planes, const int64_t*
                              const uint16_t* const* lut, const uint16_t* const* x, int m_x,
                              const int64_t* ldx, int64_t x_off, int x_split, void* const* y,
                              int y_dtype, const int64_t* ldy, int64_t y_off, int flags,
-                             cudaStream_t s) {
+                             cudaStream_t s, int m_x_total) {
     GemvLaunch L;
     L.flags = flags;
     L.n_prob = n;
@@ -1073,6 +1069,8 @@ static int gemv_launch_chunk(int n, const uint8_t* const* planes, const int64_t*
         P.planes = planes[i];
         P.lut = lut[i];
         P.x = x[i] + x_off * ldx[i];
+        // scaled pairs: the inverse scales follow the whole [m_x_total][ldx] block
+        P.xinv = x_split == 2 ? reinterpret_cast<const float*>(x[i] + (int64_t)m_x_total * ldx[i]) + x_off / 2 : nullptr;
         P.y = reinterpret_cast<uint8_t*>(y[i]) + y_off * ldy[i] * esz;
         P.rows = rows[i];
         P.cols = cols[i];
@@ -1120,6 +1118,7 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
     if (n_problems < 1) return APB_ERR_SHAPE;
     if (k < 2 || k > 8) return APB_ERR_PARAM;
     if (y_dtype != APB_DTYPE_F32 && y_dtype != APB_DTYPE_F16) return APB_ERR_PARAM;
+    if (x_split < 0 || x_split > 2) return APB_ERR_PARAM;
     if (m_x < 1 || (x_split && (m_x & 1))) return APB_ERR_SHAPE;
     const bool glu = (flags & APB_FLAG_GLU) != 0;
     for (int i = 0; i < n_problems; ++i) {
@@ -1147,7 +1146,7 @@ extern "C" int apb_gemv_grouped(int n_problems, const uint8_t* const* planes, co
             const int mc = m_x - m0 < chunk ? m_x - m0 : chunk;
             const int rc = gemv_launch_chunk(n, planes + p0, rows + p0, cols + p0, padded_cols + p0, k,
                                              lut + p0, x + p0, mc, ldx + p0, m0, x_split, y + p0,
-                                             y_dtype, ldy + p0, x_split ? m0 / 2 : m0, flags, s);
+                                             y_dtype, ldy + p0, x_split ? m0 / 2 : m0, flags, s, m_x);
             if (rc != APB_OK) return rc;
         }
     }
@@ -1169,7 +1168,7 @@ extern "C" void* apb_gemv_plan_create(int n_problems, const uint8_t* const* plan
                                       const int64_t* ldy, int flags) {
     if (n_problems < 1 || n_problems > 16 || k < 3 || k > 8) return nullptr;
     if (y_dtype != APB_DTYPE_F32 && y_dtype != APB_DTYPE_F16) return nullptr;
-    if (m_x < 1 || m_x > 16 || (x_split && (m_x & 1))) return nullptr;
+    if (x_split < 0 || x_split > 2 || m_x < 1 || m_x > 16 || (x_split && (m_x & 1))) return nullptr;
     const bool glu = (flags & APB_FLAG_GLU) != 0;
     for (int i = 0; i < n_problems; ++i) {
         if (rows[i] <= 0 || cols[i] <= 0 || (glu && (rows[i] & 1))) return nullptr;
@@ -1200,6 +1199,7 @@ extern "C" int apb_gemv_grouped_peers(int n_problems, const uint8_t* const* plan
     if (n_problems < 1) return APB_ERR_SHAPE;
     if (k < 3 || k > 8) return APB_ERR_PARAM;  // the TMA kernel's range
     if (y_dtype != APB_DTYPE_F32 && y_dtype != APB_DTYPE_F16) return APB_ERR_PARAM;
+    if (x_split < 0 || x_split > 2) return APB_ERR_PARAM;
     if (m_x < 1 || m_x > 16 || n_problems > 16 || (x_split && (m_x & 1))) return APB_ERR_SHAPE;
     if (n_peers < 0 || n_peers > 7 || (n_peers > 0 && !y_peers) || !peer_flags) return APB_ERR_PARAM;
     for (int j = 0; j <= n_peers; ++j)

@@ -82,6 +82,7 @@ struct Prob7 {
     int item_begin;
     int64_t cost_begin;
     int xid;  // problems with equal xid read the same activations (staged once)
+    const float* xinv;  // x_split == 2: inverse activation scale per output batch row
 };
 
 struct alignas(64) Launch7 {
@@ -337,7 +338,16 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
     const int first = item_at_cost(L, L.total_cost * (int64_t)blockIdx.x / gridDim.x);
     const int last = item_at_cost(L, L.total_cost * (int64_t)(blockIdx.x + 1) / gridDim.x);
     asm volatile("griddepcontrol.launch_dependents;");
-    if (first >= last) return;
+    if (first >= last) {
+        // RMSNorm producer: the consumer sums ALL n_partials slots, so a CTA
+        // without items still writes its (zero) share -- after the PDL wait: a
+        // consumer of the previous producer may read the slot until then
+        if (EPI && L.norm_mode == 1) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (tid == 0) __stcg(L.partials + blockIdx.x, 0.f);
+        }
+        return;
+    }
     if (tid == 0) APB_TL(0);
     const int n_local = last - first;
     const int NST = L.n_stages;
@@ -582,7 +592,7 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
                     for (int w = 0; w < WC; ++w) hi += r[(w * 2 * NB + 2 * m) * kRows + rl];
 #pragma unroll
                     for (int w = 0; w < WC; ++w) lo += r[(w * 2 * NB + 2 * m + 1) * kRows + rl];
-                    return hi + lo;
+                    return L.x_split == 2 ? (hi + lo) * P.xinv[m] : hi + lo;  // scaled pairs: undo 2^e
                 }
                 float sum = 0.f;
 #pragma unroll
@@ -698,6 +708,11 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
 #pragma unroll
             for (int o = 16; o; o >>= 1) sq_acc += __shfl_xor_sync(0xffffffffu, sq_acc, o);
             if (lane == 0) __stcg(L.partials + blockIdx.x, sq_acc);
+            // this grid (its size depends on k and the shape) may be smaller than
+            // the previous producer's on the same buffer: CTA 0 zeroes the slots no
+            // CTA of this grid owns (the service warp has passed the PDL wait)
+            if (blockIdx.x == 0)
+                for (int i = (int)gridDim.x + lane; i < L.n_partials; i += 32) __stcg(L.partials + i, 0.f);
         }
         if (ep_peers >= 0) {
             // publish: every lane's local + peer stores visible system-wide, then
@@ -1121,12 +1136,8 @@ static int launch(Launch7& L, int flags, cudaStream_t s) {
     if (nst < G::kNG || nst < 3) return -1;
     L.n_stages = nst;
     auto kern = gemv7_kernel<K, NB, CPS, EPI>;
-    static std::atomic<int> configured{0};
-    if (!configured.load(std::memory_order_acquire)) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit) != cudaSuccess)
-            return APB_ERR_CUDA;
-        configured.store(1, std::memory_order_release);
-    }
+    static std::atomic<unsigned long long> configured{0};
+    if (!apb::ensure_smem_optin(kern, (int)kSmemLimit, configured)) return APB_ERR_CUDA;
     int grid = CPS * sm_count();
     if (grid > L.n_items) grid = L.n_items;
     if (L.norm_mode == 1 && grid > L.n_partials) return APB_ERR_PARAM;  // a CTA without a partials slot
@@ -1188,6 +1199,25 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
 }
 
 namespace apb7 {
+// Activation identity: layers fed the same x (q/k/v, gate/up) stage it once.
+// From the problems' CURRENT x pointers (re-run when a plan is re-pointed).
+static void assign_xids(Launch7& L) {
+    int n_xid = 0;
+    for (int i = 0; i < L.n_prob; ++i) {
+        Prob7& P = L.prob[i];
+        P.xid = i;
+        for (int j = 0; j < i; ++j) {
+            const Prob7& Q = L.prob[j];
+            if (Q.x == P.x && Q.ldx == P.ldx && Q.cols == P.cols) {
+                P.xid = Q.xid;
+                break;
+            }
+        }
+        if (P.xid == i) ++n_xid;
+    }
+    L.x_bufs = n_xid == 1 ? 1 : 2;
+}
+
 // Launch7 of a call (tensor maps encoded, partition fixed); -1 when this kernel
 // does not apply.  No argument validation beyond that (the callers validate).
 int apb7_build(Launch7& L, int& nb, int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
@@ -1222,6 +1252,7 @@ int apb7_build(Launch7& L, int& nb, int n, const uint8_t* const* planes, const i
         if (!make_plane_map(&L.tm_planes[i], planes[i], n_max[i], rows[i], row_bytes)) return -1;
         if (!make_lut_map(&L.tm_lut[i], lut[i], k, rows[i])) return -1;
         P.x = x[i] + x_off * ldx[i];
+        P.xinv = x_split == 2 ? reinterpret_cast<const float*>(x[i] + (int64_t)m_x * ldx[i]) + x_off / 2 : nullptr;
         P.y = reinterpret_cast<uint8_t*>(y[i]) + y_off * ldy[i] * esz;
         for (int j = 0; j < n_peers; ++j)  // the same region of every peer's output
             L.y_peer[i][j] = reinterpret_cast<uint8_t*>(y_peers[(size_t)i * n_peers + j]) + y_off * ldy[i] * esz;
@@ -1240,18 +1271,7 @@ int apb7_build(Launch7& L, int& nb, int n, const uint8_t* const* planes, const i
     L.n_items = items;
     L.total_cost = cost;
     L.xs_bytes = (int64_t)m_x * max_tiles * 2048;
-    // activation identity: layers fed the same x (q/k/v, gate/up) stage it once
-    int n_xid = 0;
-    for (int i = 0; i < n; ++i) {
-        L.prob[i].xid = i;
-        for (int j = 0; j < i; ++j)
-            if (x[j] == x[i] && ldx[j] == ldx[i] && cols[j] == cols[i]) {
-                L.prob[i].xid = L.prob[j].xid;
-                break;
-            }
-        if (L.prob[i].xid == i) ++n_xid;
-    }
-    L.x_bufs = n_xid == 1 ? 1 : 2;
+    assign_xids(L);
     L.n_peers = peer_flags ? n_peers : -1;  // -1: no fused gather at all
     if (peer_flags)
         for (int j = 0; j <= n_peers; ++j) L.peer_flag[j] = peer_flags[j];
@@ -1320,15 +1340,19 @@ extern "C" int apb_gemv_plan_launch(void* plan, const uint16_t* const* x, void* 
     auto* p = static_cast<ApbGemvPlan7*>(plan);
     if (!p) return APB_ERR_PARAM;
     for (int i = 0; i < p->n; ++i) {
-        if (x) {
-            if (!x[i] || ((uintptr_t)x[i] & 15)) return APB_ERR_PARAM;
-            p->L.prob[i].x = x[i];
-        }
-        if (y) {
-            if (!y[i]) return APB_ERR_PARAM;
-            p->L.prob[i].y = y[i];
-        }
+        if (x && (!x[i] || ((uintptr_t)x[i] & 15))) return APB_ERR_PARAM;
+        if (y && !y[i]) return APB_ERR_PARAM;
     }
+    for (int i = 0; i < p->n; ++i) {
+        apb7::Prob7& P = p->L.prob[i];
+        if (x) {
+            P.x = x[i];
+            if (p->L.x_split == 2) P.xinv = reinterpret_cast<const float*>(x[i] + (int64_t)p->L.m_x * P.ldx);
+        }
+        if (y) P.y = y[i];
+    }
+    // the staging decision (one shared x buffer or two) follows the new pointers
+    if (x) apb7::assign_xids(p->L);
     return apb7::apb7_dispatch(p->L, p->k, p->nb, p->flags, (cudaStream_t)stream);
 }
 

@@ -220,9 +220,40 @@ def _ldx(cols: int) -> int:
     return -(-cols // 8) * 8
 
 
+def _split_tail_halves(m: int) -> int:
+    """fp16 elements that hold the m fp32 inverse scales behind a scaled-pair
+    block (x_split = 2), rounded up to 16 bytes."""
+    return -(-2 * m // 8) * 8
+
+
+def _split_scaled_np(x32: np.ndarray, ldx: int) -> np.ndarray:
+    """Host restatement of apb_split_x_scaled (csrc/apb_dense.cu): flat fp16
+    [2m*ldx + tail] = (hi, lo) row pairs of x * s_r followed by float32 1/s_r,
+    s_r the power of two putting row r's max |x| in [2^14, 2^15)."""
+    m, cols = x32.shape
+    out = np.zeros(2 * m * ldx + _split_tail_halves(m), dtype=np.float16)
+    rows = out[: 2 * m * ldx].reshape(2 * m, ldx)
+    inv = np.ones(m, dtype=np.float32)
+    for r in range(m):
+        a = float(np.max(np.abs(x32[r]))) if cols else 0.0
+        scale = np.float32(1.0)
+        if a > 0.0 and np.isfinite(a):
+            e = int(np.frexp(np.float32(a))[1])
+            scale = np.float32(np.ldexp(np.float32(1.0), min(max(15 - e, -126), 126)))
+        v = x32[r] * scale  # exact: a power of two
+        hi = v.astype(np.float16)
+        rows[2 * r, :cols] = hi
+        rows[2 * r + 1, :cols] = (v - hi.astype(np.float32)).astype(np.float16)
+        inv[r] = np.float32(1.0) / scale
+    out[2 * m * ldx:2 * m * ldx + 2 * m] = inv.view(np.float16)
+    return out
+
+
 def _stage_x(x, cols: int, fp16: bool):
     """_prep_x (engine.py:270-281) for the GPU: returns (xdev fp16 [m_x][ldx],
-    m_x, ldx, split, host_kind).  fp32 activations become (hi, lo) fp16 pairs."""
+    m_x, ldx, split, host_kind).  fp32 activations become scaled (hi, lo) fp16
+    pairs (x_split = 2: the block carries its inverse row scales behind the
+    rows, so any fp32 magnitude keeps ~22 significant bits)."""
     torch = dev.require_cuda()
     ldx = _ldx(cols)
     if dev.is_tensor(x):
@@ -239,23 +270,18 @@ def _stage_x(x, cols: int, fp16: bool):
             buf[:, :cols] = x2
             return buf, m, ldx, 0, kind
         x32 = x2.to(torch.float32).contiguous()
-        buf = torch.empty((2 * m, ldx), dtype=torch.float16, device=x2.device)
-        check(load().apb_split_x(dev.ptr(x32), m, cols, cols, dev.ptr(buf), ldx, 0,
-                                 dev.stream_ptr()), "apb_split_x")
-        return buf, 2 * m, ldx, 1, kind
+        flat = torch.empty(2 * m * ldx + _split_tail_halves(m), dtype=torch.float16, device=x2.device)
+        check(load().apb_split_x_scaled(dev.ptr(x32), m, cols, cols, dev.ptr(flat), ldx,
+                                        dev.stream_ptr()), "apb_split_x_scaled")
+        return flat[: 2 * m * ldx].view(2 * m, ldx), 2 * m, ldx, 2, kind
     x = np.asarray(x)
     m = x.shape[0]
     if fp16 or x.dtype == np.float16:
         h = np.zeros((m, ldx), dtype=np.float16)
         h[:, :cols] = x.astype(np.float16)
         return dev.to_device(h), m, ldx, 0, "numpy"
-    x32 = x.astype(np.float32)
-    hi = x32.astype(np.float16)
-    lo = (x32 - hi.astype(np.float32)).astype(np.float16)
-    h = np.zeros((2 * m, ldx), dtype=np.float16)
-    h[0::2, :cols] = hi
-    h[1::2, :cols] = lo
-    return dev.to_device(h), 2 * m, ldx, 1, "numpy"
+    flat = dev.to_device(_split_scaled_np(x.astype(np.float32), ldx))
+    return flat[: 2 * m * ldx].view(2 * m, ldx), 2 * m, ldx, 2, "numpy"
 
 
 class _CallPlan:
@@ -270,9 +296,13 @@ class _CallPlan:
         t = prep.tensor
         self.m_x, self.split, self.ldx = m_x, split, _ldx(t.cols)
         self.m_out = m_x // 2 if split else m_x
-        self.x = torch.zeros((m_x, self.ldx), dtype=torch.float16, device="cuda")
+        # scaled pairs (split = 2) carry their inverse row scales behind the rows
+        n_x = m_x * self.ldx + (_split_tail_halves(self.m_out) if split == 2 else 0)
+        self._x_flat = torch.zeros(n_x, dtype=torch.float16, device="cuda")
+        self._x_pin_flat = torch.zeros(n_x, dtype=torch.float16, pin_memory=True)
+        self.x = self._x_flat[: m_x * self.ldx].view(m_x, self.ldx)
         self.y = torch.empty((self.m_out, t.rows), dtype=torch.float32, device="cuda")
-        self.x_pin = torch.zeros((m_x, self.ldx), dtype=torch.float16, pin_memory=True)
+        self.x_pin = self._x_pin_flat[: m_x * self.ldx].view(m_x, self.ldx)
         self.y_pin = torch.empty((self.m_out, t.rows), dtype=torch.float32, pin_memory=True)
         self._lib = load()
         PP = lambda a: ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))  # noqa: E731
@@ -292,7 +322,8 @@ class _CallPlan:
         self.x_ptr, self.y_ptr = dev.ptr(self.x), dev.ptr(self.y)
         self.x_pin_ptr, self.y_pin_ptr = dev.ptr(self.x_pin), dev.ptr(self.y_pin)
         self.x_np, self.y_np = self.x_pin.numpy(), self.y_pin.numpy()
-        self.x_bytes, self.y_bytes = self.x.numel() * 2, self.y.numel() * 4
+        self.x_flat_np = self._x_pin_flat.numpy()
+        self.x_bytes, self.y_bytes = self._x_flat.numel() * 2, self.y.numel() * 4
         self._host_graph = None  # H2D -> launch -> D2H captured once (host_graph())
         self._host_graph_failed = False
 
@@ -338,16 +369,12 @@ class _CallPlan:
 
 
 def _host_rows(x, m: int, fp16: bool):
-    """Host activation block -> its staged fp16 rows (m_x, split) as numpy."""
+    """Host activation block -> (staged fp16 rows or, for fp32 activations,
+    the flat scaled-pair block of apb_split_x_scaled for ldx, m_x, split)."""
     x = x.numpy() if dev.is_tensor(x) else np.asarray(x)
     if fp16 or x.dtype == np.float16:
         return x.astype(np.float16), m, 0
-    x32 = x.astype(np.float32)
-    hi = x32.astype(np.float16)
-    lo = (x32 - hi.astype(np.float32)).astype(np.float16)
-    h = np.empty((2 * m, x.shape[1]), dtype=np.float16)
-    h[0::2], h[1::2] = hi, lo
-    return h, 2 * m, 1
+    return _split_scaled_np(x.astype(np.float32), _ldx(x.shape[1])), 2 * m, 2
 
 
 def _quantized(prep: PreparedLayer, x2, k: int, fp16: bool):
@@ -362,7 +389,10 @@ def _quantized(prep: PreparedLayer, x2, k: int, fp16: bool):
         rows16, m_x, split = _host_rows(x2, m, fp16)
         plan = prep._call_plan(k, m_x, split)
         if plan.handle is not None:
-            plan.x_np[:, :t.cols] = rows16
+            if split == 2:
+                plan.x_flat_np[:] = rows16  # whole block: pairs + inverse scales
+            else:
+                plan.x_np[:, :t.cols] = rows16
             lib, g = plan._lib, plan.host_graph()
             if g is not None:
                 g.replay()  # on the current stream

@@ -72,6 +72,11 @@ class GemvPlan:
         if norm is not None:
             from ._lib import NormEpilogue
 
+            # apb_gemv_grouped_norm has no hi/lo activation pairs: its m_x rows are
+            # batch rows, so a split plan would write 2m output rows into y [m][R]
+            if x_split:
+                raise ParameterError("a norm epilogue cannot be combined with x_split activations")
+
             if norm[0] == "producer":
                 _, resid, w, part = norm
                 self._norm = NormEpilogue(1, dev.ptr(resid), dev.ptr(w), dev.ptr(part), part.numel(), 0, 0.0)

@@ -204,40 +204,44 @@ def continue_upscale(weights, sens, layer, new_n_max: int, *, row_block: int | N
 # ---- the rest of the reference quantizer module (quantizer.py:31-72, 122-307) ----
 
 class SensitivityMap:
-    """Per-weight non-negative importance, same shape as the weight matrix
-    (quantizer.py:31-47)."""
+    """Importance of every weight (float64, the weight matrix's shape, >= 0),
+    as the reference's quantizer.py:31-47 defines it; ``fallback`` marks maps
+    that were synthesised from degenerate calibration data."""
 
     def __init__(self, values, fallback: bool = False):
-        self.values = np.asarray(values, dtype=np.float64)
-        self.fallback = fallback
-        if self.values.ndim != 2:
-            raise ShapeError("sensitivity map must be 2-D")
-        if np.any(self.values < 0):
-            raise ParameterError("sensitivity values must be non-negative")
+        v = np.asarray(values, dtype=np.float64)
+        _require(v.ndim == 2, ShapeError, "sensitivity map must be 2-D")
+        _require(not np.any(v < 0), ParameterError, "sensitivity values must be non-negative")
+        self.values, self.fallback = v, fallback
 
     @classmethod
     def uniform(cls, shape, fallback: bool = False) -> "SensitivityMap":
-        return cls(np.ones(shape, dtype=np.float64), fallback=fallback)
+        return cls(np.full(shape, 1.0), fallback=fallback)
+
+
+def _require(ok: bool, exc, msg: str) -> None:
+    """Raise the reference's exception class / message when a check fails."""
+    if not ok:
+        raise exc(msg)
 
 
 class ChannelQuantization:
-    """One channel's codes and sorted float64 centroids at one bit-width
-    (quantizer.py:50-72)."""
+    """A channel quantized at one bit-width: integer codes and its 2^k sorted
+    float64 centroids (data contract of quantizer.py:50-72)."""
 
     def __init__(self, bit_width: int, codes, centroids):
-        self.bit_width = bit_width
-        self.codes = np.asarray(codes)
-        self.centroids = np.asarray(centroids, dtype=np.float64)
         k = bit_width
-        if not MIN_BITS <= k <= MAX_BITS:
-            raise ParameterError(f"bit width {k} outside [{MIN_BITS}, {MAX_BITS}]")
-        if self.centroids.shape != (1 << k,):
-            raise ShapeError(f"expected {1 << k} centroids for {k}-bit channel, got {self.centroids.shape}")
-        if self.codes.size and (self.codes.min() < 0 or self.codes.max() >= (1 << k)):
-            raise ParameterError("codes out of range for bit width")
+        c = np.asarray(codes)
+        cent = np.asarray(centroids, dtype=np.float64)
+        _require(MIN_BITS <= k <= MAX_BITS, ParameterError, f"bit width {k} outside [{MIN_BITS}, {MAX_BITS}]")
+        _require(cent.shape == (1 << k,), ShapeError,
+                 f"expected {1 << k} centroids for {k}-bit channel, got {cent.shape}")
+        _require(c.size == 0 or (c.min() >= 0 and c.max() < (1 << k)), ParameterError,
+                 "codes out of range for bit width")
+        self.bit_width, self.codes, self.centroids = k, c, cent
 
     def dequantized(self) -> np.ndarray:
-        return self.centroids[self.codes]
+        return np.take(self.centroids, self.codes)
 
 
 class KMeans1DResult(tuple):
@@ -253,28 +257,29 @@ class KMeans1DResult(tuple):
 
 
 def estimate_sensitivity_diag(gradient_samples, shape=None) -> SensitivityMap:
-    """Elementwise mean of squared gradient samples (quantizer.py:160-187):
-    host-side statistics of the calibration gradients, same fallbacks."""
-    samples = [np.asarray(g, dtype=np.float64) for g in gradient_samples]
-    if not samples:
-        if shape is None:
-            raise ParameterError("empty sample list needs an explicit shape for the fallback")
-        log.warning("no gradient samples; using uniform sensitivity")
+    """Diagonal-Fisher importance: per weight, the mean over the calibration
+    samples of the squared gradient (behaviour of quantizer.py:160-187).  The
+    squares are accumulated sample after sample in float64 and divided once,
+    the reference's order, so the map matches it bit for bit.  With no samples
+    the map is uniform over ``shape``; rows whose mean is zero everywhere
+    become uniform rows; either case sets ``fallback``."""
+    grads = [np.asarray(g, dtype=np.float64) for g in gradient_samples]
+    if len(grads) == 0:
+        _require(shape is not None, ParameterError, "empty sample list needs an explicit shape for the fallback")
+        log.warning("estimate_sensitivity_diag: no gradient samples, uniform importance")
         return SensitivityMap.uniform(shape, fallback=True)
-    shape = samples[0].shape
-    for g in samples[1:]:
-        if g.shape != shape:
-            raise ShapeError("gradient samples must share one shape")
-    acc = np.zeros(shape, dtype=np.float64)
-    for g in samples:
-        acc += g * g
-    acc /= len(samples)
-    dead = ~np.any(acc > 0, axis=1)
-    if np.any(dead):
-        log.warning("uniform sensitivity fallback for %d all-zero channel(s)", dead.sum())
-        acc[dead] = 1.0
-        return SensitivityMap(acc, fallback=True)
-    return SensitivityMap(acc)
+    first = grads[0].shape
+    _require(all(g.shape == first for g in grads), ShapeError, "gradient samples must share one shape")
+    fisher = np.zeros(first, dtype=np.float64)
+    for g in grads:
+        np.add(fisher, np.square(g), out=fisher)
+    fisher /= len(grads)
+    zero_rows = np.flatnonzero(~(fisher > 0).any(axis=1))
+    if zero_rows.size == 0:
+        return SensitivityMap(fisher)
+    log.warning("estimate_sensitivity_diag: %d channel(s) without gradient signal -> uniform", zero_rows.size)
+    fisher[zero_rows] = 1.0
+    return SensitivityMap(fisher, fallback=True)
 
 
 def _cluster_device(torch, w, s, k: int):

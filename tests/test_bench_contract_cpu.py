@@ -50,3 +50,61 @@ def test_metric_matches_baseline_json():
     with open(os.path.join(ROOT, "BASELINE.json")) as f:
         base = json.load(f)
     assert bench.METRIC == base["metric"]
+
+
+def test_gpus_flag_spawns_ranks_gloo():
+    """`bench.py --gpus 2` with no launcher re-executes itself under
+    torch.distributed.run with 2 ranks (here the --dry-run plumbing: gloo
+    all-reduce of the ranks, rank 0 prints the line)."""
+    import subprocess
+    import sys
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["rank_sum"] == 1 and d["gpus_arg"] == 2
+
+
+def test_gpus_flag_mismatch_refused():
+    import subprocess
+    import sys
+
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr
+
+
+def test_gpus_flag_refused_without_devices():
+    """A box with fewer GPUs than --gpus refuses loudly instead of running one
+    rank and reporting n_gpus 1."""
+    import subprocess
+    import sys
+
+    import torch
+
+    if torch.cuda.device_count() >= 2:
+        return
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 3 and "refusing" in out.stderr
+
+
+def test_l2_clean_rotation():
+    """The headline's copy rotation: within a step no launch group reads the
+    same copy at two bit-widths closer than 4 apart, and every copy is used."""
+    import bench
+
+    seen = {}
+    for ki in range(len(bench.BITS)):
+        for gi in range(len(bench.GROUPS)):
+            c = bench.copy_index(ki, gi)
+            if (gi, c) in seen:
+                assert ki - seen[(gi, c)] >= 4
+            seen[(gi, c)] = ki
+    assert {c for _, c in seen} == set(range(bench.N_COPIES))

@@ -54,7 +54,7 @@ def test_decode_step_matches_dequantized_reference():
         got = model.hbuf.float().view(-1)
         want = _reference_hidden(torch, engine, model, k)
         err = float((got - want).norm() / want.norm())
-        assert err < 2e-2, (k, err)
+        assert err < 1e-2, (k, err)  # north_star's bar
         model.capture(k)  # graph replay gives the same bits
         model.step(k)
         torch.cuda.synchronize()
@@ -199,10 +199,13 @@ def test_decode_step_llama7b_block_shapes():
     cfg = LlamaConfig(layers=2, vocab=1000)
     model = DecodeModel(cfg, context=256, seed=5)
     model.token.fill_(123)
-    for k in (3, 6):
+    # k = 6 -> 7 -> 8 on ONE model: the RMSNorm producers' grids shrink (down:
+    # 256 -> 148 CTAs, o: 256 -> 148 at k = 8), so partial-sum slots the smaller
+    # grid does not own must not keep the previous k's values
+    for k in (3, 6, 7, 8, 6):
         model.step(k)
         torch.cuda.synchronize()
         got = model.hbuf.float().view(-1)
         want = _reference_hidden(torch, engine, model, k)
         err = float((got - want).norm() / want.norm())
-        assert err < 2e-2, (k, err)
+        assert err < 1e-2, (k, err)  # north_star's bar

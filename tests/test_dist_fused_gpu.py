@@ -233,9 +233,17 @@ def test_fused_allgather_llama70b_shapes(layers70b, world, k):
             want = torch.cat([refs[r].y[i] for r in range(world)], dim=1)
             for r in range(world):
                 assert torch.equal(plans[r].y[i], want), (name, r, i)
-        y_full = engine.gemv(engine.prepare(layers[-1]), x[0], engine.GemvConfig(bit_width=k, activations_fp16=True))
-        err = float((plans[world - 1].y[-1][0].float() - y_full.float()).norm() / y_full.float().norm())
-        assert err < 2e-3, (name, err)
+        # the gathered fp16 outputs against the C oracle on the UNSHARDED layer:
+        # within fp16 output rounding (the payload of the all-gather is fp16)
+        xh = x[0].float().cpu().numpy()
+        for i, L in enumerate(layers):
+            planes = ora.permute(ora.pack_bitplanes(L.codes, 8))
+            want = ora.gemm(planes, cols, k, L.centroid_tables[k], ora.prep_x(xh, cols, True), nthreads=8)
+            want16 = want.astype(np.float16).astype(np.float32)
+            for r in range(world):
+                got = plans[r].y[i][0].float().cpu().numpy()
+                err = ora.rel_err(got, want16)
+                assert err < 1e-3, (name, i, r, err)
         for gt in gathers:
             gt.close()
         del plans, refs, shard_preps

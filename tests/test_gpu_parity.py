@@ -253,6 +253,64 @@ def test_gemv_llama7b_shapes_vs_oracle(api, shape):
         assert ora.rel_err(y16, want16) < TOL, (shape, k)
 
 
+@pytest.mark.parametrize("shape", [(8192, 8192), (28672, 8192), (8192, 28672)])
+def test_gemv_llama70b_shapes_vs_oracle(api, shape):
+    # BASELINE configs[3] shapes, unsharded, against the C oracle on 8 host
+    # threads (test_engine.py:149-156's bar): the GPU packer bit-exact against the
+    # oracle's CPU packing at 235 MB, then gemv at k = 3 / 6 / 8 with fp32
+    # (scaled hi/lo pairs) and fp16 activations
+    _, _, engine, _ = api
+    rows, cols = shape
+    layer = _random_layer(api, 700 + rows + cols, rows, cols)
+    prep = engine.prepare(layer)
+    planes = prep.planes.cpu().numpy()
+    assert np.array_equal(planes, ora.permute(ora.pack_bitplanes(layer.codes, 8))), shape
+    x = np.random.default_rng(rows).standard_normal(cols)
+    for k in (3, 6, 8):
+        t = layer.centroid_tables[k]
+        for fp16 in (False, True):
+            want = ora.gemm(planes, cols, k, t, ora.prep_x(x, cols, fp16), nthreads=8)
+            y = engine.gemv(prep, x, engine.GemvConfig(bit_width=k, activations_fp16=fp16))
+            assert ora.rel_err(y, want) < TOL, (shape, k, fp16, ora.rel_err(y, want))
+
+
+@pytest.mark.parametrize("scale", [1e-30, 1e-6, 1.0, 3e4, 1e5, 1e30])
+def test_fp32_activation_magnitudes(api, scale):
+    # fp32 activations of any magnitude (engine.py:270-281 keeps them fp32): the
+    # hi/lo pairs are taken after a power-of-two row scale (x_split = 2), so
+    # |x| >= 65520 does not overflow fp16 and tiny rows keep ~22 bits; rows of
+    # one batch may differ by 60 orders of magnitude, an all-zero row stays zero
+    _, _, engine, _ = api
+    rows, cols = 700, 3000
+    layer = _random_layer(api, 123, rows, cols)
+    prep = engine.prepare(layer)
+    planes = prep.planes.cpu().numpy()
+    rng = np.random.default_rng(int(abs(np.log10(scale))) + 5)
+    x = (rng.standard_normal((4, cols)) * scale).astype(np.float32)
+    x[1] *= 1e-20 if scale > 1 else 1e20
+    x[2] = 0.0
+    for k in (3, 5, 8):
+        want = ora.gemm(planes, cols, k, layer.centroid_tables[k], ora.prep_x(x, cols, False))
+        for m in (1, 2, 4):  # row-copy and batch-in-N mappings
+            y = engine.gemm(prep, x[:m], engine.GemvConfig(bit_width=k))
+            assert np.all(np.isfinite(y)), (scale, k, m)
+            for r in range(m):
+                if r == 2:
+                    assert not np.any(y[r]), (scale, k)
+                    continue
+                assert ora.rel_err(y[r], want[r]) < TOL, (scale, k, m, r, ora.rel_err(y[r], want[r]))
+        yv = engine.gemv(prep, x[0], engine.GemvConfig(bit_width=k))  # per-call host path
+        assert ora.rel_err(yv, want[0]) < TOL, (scale, k)
+    import torch
+
+    xd = torch.from_numpy(x).cuda()  # device path: apb_split_x_scaled
+    yd = engine.gemm(prep, xd, engine.GemvConfig(bit_width=4))
+    want = ora.gemm(planes, cols, 4, layer.centroid_tables[4], ora.prep_x(x, cols, False))
+    for r in (0, 1, 3):
+        assert ora.rel_err(yd[r].cpu().numpy(), want[r]) < TOL, (scale, r)
+    assert not torch.any(yd[2])
+
+
 @pytest.mark.parametrize("m", [1, 2, 4, 8, 16, 40])
 def test_small_batch_gemm_vs_oracle(api, m):
     _, _, engine, _ = api
@@ -398,6 +456,55 @@ def test_device_tensors_stay_on_device(api):
     y16 = engine.gemv(prep, x16, engine.GemvConfig(bit_width=4))
     y16b = engine.gemv(prep, x16.float(), engine.GemvConfig(bit_width=4, activations_fp16=True))
     assert torch.equal(y16, y16b)
+
+
+def test_plan_relaunch_with_new_activation_pattern(api):
+    # apb_gemv_plan_launch may re-point a plan created with ONE x shared by both
+    # layers at two distinct x buffers (and back): the shared-activation staging
+    # follows the pointers of each launch, so layer 1 never reuses layer 0's x
+    import ctypes
+
+    import torch
+
+    from paper_2402_10517_b200 import _device as dev
+    from paper_2402_10517_b200._lib import APB_DTYPE_F32, check, int64_array, int_array, load, ptr_array
+
+    _, _, engine, _ = api
+    preps = [engine.prepare(_random_layer(api, 40 + i, 512, 2048)) for i in range(2)]
+    lib, k = load(), 4
+    PP = lambda a: ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))  # noqa: E731
+    xs = torch.randn(1, 2048, device="cuda").half()
+    xa, xb = torch.randn(1, 2048, device="cuda").half(), torch.randn(1, 2048, device="cuda").half()
+    ys = [torch.zeros(1, 512, device="cuda") for _ in range(2)]
+    keep = [ptr_array([dev.ptr(p.planes) for p in preps]), int_array([8, 8]), int64_array([512, 512]),
+            int64_array([2048, 2048]), int64_array([2048, 2048]), ptr_array([dev.ptr(p.tables16[k]) for p in preps]),
+            ptr_array([dev.ptr(xs), dev.ptr(xs)]), int64_array([2048, 2048]), ptr_array([dev.ptr(y) for y in ys])]
+    pl, nm, rw, cl, pd, lt, xp, lx, yp = keep
+    h = lib.apb_gemv_plan_create(2, PP(pl), nm, rw, cl, pd, k, PP(lt), PP(xp), 1, lx, 0, PP(yp), APB_DTYPE_F32,
+                                 int64_array([512, 512]), 0)
+    assert h
+    try:
+        for pair in ((xa, xb), (xs, xs), (xb, xa)):
+            check(lib.apb_gemv_plan_launch(h, PP(ptr_array([dev.ptr(t) for t in pair])), None, dev.stream_ptr()),
+                  "apb_gemv_plan_launch")
+            torch.cuda.synchronize()
+            for p, xx, y in zip(preps, pair, ys):
+                want = engine.gemv(p, xx[0], engine.GemvConfig(bit_width=k))
+                assert torch.equal(y[0], want)
+    finally:
+        lib.apb_gemv_plan_destroy(h)
+
+
+def test_norm_plan_rejects_split_activations(api):
+    import torch
+
+    from paper_2402_10517_b200 import plan
+
+    _, _, engine, errors = api
+    prep = engine.prepare(_random_layer(api, 9, 64, 1024))
+    part = torch.zeros(320, device="cuda")
+    with pytest.raises(errors.ParameterError):
+        plan.GemvPlan([prep], 4, x_split=True, norm=("consumer", part, 1024, 1e-5))
 
 
 def test_grouped_equals_single(api):
