@@ -12,10 +12,10 @@ dependent launch and replayed from a CUDA graph.
 value: whole-job algorithmic HBM GB/s = sum of SURVEY.md section 8(d) bytes
 (R*C*k/8 + R*2^k*2 + C*2 + R*2 per GEMV) / device time (CUDA events on the
 launch stream, max over ranks).  Inputs are resident in HBM and larger than
-L2 by construction: 4 full copies of the layer set (4 x 203 MB), and launch
-(k_i, group g) reads copy (g + k_i) mod 4, so a layer's planes are re-read only
-4 bit-widths later with >= 3 whole bit-width sets (> 300 MB, > 2x the 126 MB
-L2) read in between; every detail leg rotates over > 2x L2 of distinct bytes.
+L2 by construction: 6 full copies of the layer set (6 x 203 MB), and launch
+(k_i, group g) reads copy (g + k_i) mod 6, so a launch group re-reads the same
+planes only one whole step (> 870 MB, > 6x the 126 MB L2) later; every detail
+leg rotates over > 2x L2 of distinct bytes.
 With N > 1 GPUs every layer is row-sharded (rank i holds rows
 [i*R/N, (i+1)*R/N)) and each GEMV's output slices are all-gathered (fused into
 the GEMV epilogue over NVLink P2P, or NCCL) -- strong scaling: total work
@@ -50,7 +50,7 @@ SHAPES = [("q", 4096, 4096), ("k", 4096, 4096), ("v", 4096, 4096), ("o", 4096, 4
 GROUPS = [[0, 1, 2], [3], [4, 5], [6]]  # decode-block launch groups (shared x within a group)
 BITS = [3, 4, 5, 6, 7, 8]
 N_MAX = 8
-N_COPIES = 4
+N_COPIES = 6
 METRIC = "bitplane GEMV µs & HBM GB/s (% roofline) at k=3..8, Llama-2-7B layer shapes"
 
 
@@ -156,8 +156,9 @@ def make_layer_set(torch, seed: int, rank: int = 0, world: int = 1):
 
 def copy_index(ki: int, gi: int) -> int:
     """Weight copy read by launch group gi at bit-width index ki: group g cycles
-    through the copies as k grows, so the same planes come back only 4
-    bit-widths later (>= 3 full bit-width sets, > 300 MB, read in between)."""
+    through all 6 copies as k goes 3..8, so a launch group never re-reads the
+    same planes within a step, and across steps only after a whole step
+    (> 870 MB) of other planes."""
     return (gi + ki) % N_COPIES
 
 
@@ -253,27 +254,21 @@ def time_graph(torch, fn, reps: int):
 
 
 def measured_traffic():
-    """roofline.traffic: DRAM bytes (ncu dram__bytes_read.sum + write.sum) of the
-    GEMV launches captured by `ncu --set full` (tools/gpu_bench_profile.sh ->
-    profiles/r1_traffic.json: one k-group qkv | o | gate+up | down), scaled to
-    one step by their algorithmic bytes.  None when no capture is committed."""
+    """roofline.traffic: DRAM bytes (dram__bytes_read.sum + write.sum) per
+    average GEMV launch of the TIMED launch pattern, from the committed
+    `ncu --cache-control none` capture of whole bench steps (caches in their
+    natural state between launches; tools/gpu_r2.sh -> tools/traffic_summary.py
+    -> profiles/r2_traffic.json).  None when no capture is committed."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
             tr = json.load(f)
-        dram = [l["dram_bytes"] for l in tr["launches"]]
-        if len(dram) != len(GROUPS):
-            return None, None
-        k = int(tr["launches"][0]["kernel"].split("<")[1].split(">")[0].split(",")[0])
-        alg = [sum(alg_bytes(SHAPES[j][1], SHAPES[j][2], k) for j in grp) for grp in GROUPS]
-        ratio = sum(dram) / sum(alg)
+        ratio = float(tr["dram_over_algorithmic"])
         launches = len(BITS) * len(GROUPS)
-        # per launch, like `achieved`: the average GEMV launch of a step
         return round(ratio * step_bytes() / launches), {
-            "dram_over_algorithmic": round(ratio, 4), "k": k, "source": tr["source"],
+            "dram_over_algorithmic": ratio, "source": tr["source"], "steps_captured": tr["steps"],
+            "per_launch_ratio_range": [tr["min_launch_ratio"], tr["max_launch_ratio"]],
             "algorithmic_bytes_per_launch": round(step_bytes() / launches),
-            "dram_bytes_per_step": round(ratio * step_bytes()),
-            "captured_launches": [{"group": "+".join(SHAPES[j][0] for j in grp), "dram_bytes": d, "alg_bytes": a}
-                                  for grp, d, a in zip(GROUPS, dram, alg)]}
+            "dram_bytes_per_step": round(ratio * step_bytes())}
     except Exception:
         return None, None
 
@@ -403,8 +398,8 @@ def run_ours(args):
                    "launches_per_step": len(plans), "cuda_graph": graph is not None,
                    "l2": (f"inputs > L2 by construction: {N_COPIES} copies of the layer set "
                           f"({N_COPIES} x 203 MB), launch (k_i, group g) reads copy (g + k_i) mod {N_COPIES}: "
-                          "a layer's planes return only 4 bit-widths later, after >= 3 full bit-width "
-                          "sets (> 300 MB > 2x L2); planes loaded L2::evict_first")},
+                          "a launch group re-reads the same planes only one full step (> 870 MB, > 6x L2) "
+                          "later; planes loaded L2::evict_first")},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": round(value, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(value / peak, 4), "peak_kind": peak_kind,
@@ -413,7 +408,8 @@ def run_ours(args):
                      "note": "achieved = algorithmic bytes per GEMV launch / average launch time (CUDA "
                              "events over the timed region, every launch in it is the GEMV kernel: "
                              "= step bytes / step time); traffic = DRAM bytes per average launch from "
-                             "the committed ncu --set full capture (dram_over_algorithmic x algorithmic)"},
+                             "the committed ncu --cache-control none capture of the timed launch pattern "
+                             "(dram_over_algorithmic x algorithmic)"},
         "clocks": clocks,
     }
     if args.profile:
@@ -820,8 +816,7 @@ def packer_detail(torch):
 
 def grouped_all7(torch, plan, copies):
     ps = [plan.GemvPlan(copies[j % N_COPIES], k, grouped=True, pdl=True) for j, k in enumerate(BITS)]
-    # (6 launches over 4 copies: k and k+4 share a copy with the k+1..k+3 sets,
-    # > 300 MB, read in between)
+    # (6 launches over 6 copies: every launch reads its own copy)
 
     def step():
         for p in ps:

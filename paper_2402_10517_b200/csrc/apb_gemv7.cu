@@ -1127,13 +1127,14 @@ static int choose_cps(const Launch7& L) {
 }
 
 template <int K, int NB, int CPS, bool EPI>
-static int launch(Launch7& L, int flags, cudaStream_t s) {
+static int launch(Launch7& L, int flags, cudaStream_t s, bool dry = false) {
     using G = Geo<K, NB, CPS>;
     const size_t limit = CPS == 2 ? kSmemLimit2 : kSmemLimit;
     // ring depth: as many stages as fit (>= 3)
     int nst = kMaxStages;
     while (nst >= G::kNG && G::total(nst, L.x_bufs * L.xs_bytes) > limit) --nst;
     if (nst < G::kNG || nst < 3) return -1;
+    if (dry) return APB_OK;  // apb7_plan_create: the launch shape fits
     L.n_stages = nst;
     auto kern = gemv7_kernel<K, NB, CPS, EPI>;
     static std::atomic<unsigned long long> configured{0};
@@ -1173,7 +1174,7 @@ int apb7_build(Launch7& L, int& nb, int n, const uint8_t* const* planes, const i
                const uint16_t* const* x, int m_x, const int64_t* ldx, int64_t x_off, int x_split, void* const* y,
                int y_dtype, const int64_t* ldy, int64_t y_off, int flags, int n_peers, void* const* y_peers,
                uint32_t* const* peer_flags, const apb_norm_epilogue* norm);
-int apb7_dispatch(Launch7& L, int k, int nb, int flags, cudaStream_t s);
+int apb7_dispatch(Launch7& L, int k, int nb, int flags, cudaStream_t s, bool dry);
 }  // namespace apb7
 
 extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_max, const int64_t* rows,
@@ -1195,7 +1196,7 @@ extern "C" int apb7_try_gemv(int n, const uint8_t* const* planes, const int* n_m
     const int rc = apb7::apb7_build(L, nb, n, planes, n_max, rows, cols, padded, k, lut, x, m_x, ldx, x_off, x_split, y,
                                     y_dtype, ldy, y_off, flags, n_peers, y_peers, peer_flags, norm);
     if (rc != 0) return rc;
-    return apb7::apb7_dispatch(L, k, nb, flags, (cudaStream_t)stream);
+    return apb7::apb7_dispatch(L, k, nb, flags, (cudaStream_t)stream, false);
 }
 
 namespace apb7 {
@@ -1286,10 +1287,11 @@ int apb7_build(Launch7& L, int& nb, int n, const uint8_t* const* planes, const i
     return 0;
 }
 
-int apb7_dispatch(Launch7& L, int k, int nb, int flags, cudaStream_t s) {
+int apb7_dispatch(Launch7& L, int k, int nb, int flags, cudaStream_t s, bool dry) {
     const bool epi = L.glu || L.norm_mode || L.n_peers >= 0;
     switch (k * 16 + nb) {
-#define APB7_L(K, NB, CPS) (epi ? launch<K, NB, CPS, true>(L, flags, s) : launch<K, NB, CPS, false>(L, flags, s))
+#define APB7_L(K, NB, CPS) \
+    (epi ? launch<K, NB, CPS, true>(L, flags, s, dry) : launch<K, NB, CPS, false>(L, flags, s, dry))
 #define APB7_CASE(K)                                                           \
     case K * 16 + 1: return choose_cps<K, 1>(L) == 2 ? APB7_L(K, 1, 2) : APB7_L(K, 1, 1); \
     case K * 16 + 2: return APB7_L(K, 2, 1);                                    \
@@ -1324,7 +1326,8 @@ extern "C" void* apb7_plan_create(int n, const uint8_t* const* planes, const int
     if (!p) return nullptr;
     int nb = 0;
     if (apb7::apb7_build(p->L, nb, n, planes, n_max, rows, cols, padded, k, lut, x, m_x, ldx, 0, x_split, y, y_dtype,
-                         ldy, 0, flags, 0, nullptr, nullptr, nullptr) != 0) {
+                         ldy, 0, flags, 0, nullptr, nullptr, nullptr) != 0 ||
+        apb7::apb7_dispatch(p->L, k, nb, flags, nullptr, true) != APB_OK) {  // e.g. x too large to stage
         delete p;
         return nullptr;
     }
@@ -1353,7 +1356,8 @@ extern "C" int apb_gemv_plan_launch(void* plan, const uint16_t* const* x, void* 
     }
     // the staging decision (one shared x buffer or two) follows the new pointers
     if (x) apb7::assign_xids(p->L);
-    return apb7::apb7_dispatch(p->L, p->k, p->nb, p->flags, (cudaStream_t)stream);
+    const int rc = apb7::apb7_dispatch(p->L, p->k, p->nb, p->flags, (cudaStream_t)stream, false);
+    return rc == -1 ? APB_ERR_PARAM : rc;  // the re-pointed x no longer fits the staging buffers
 }
 
 extern "C" void apb_gemv_plan_destroy(void* plan) { delete static_cast<ApbGemvPlan7*>(plan); }
