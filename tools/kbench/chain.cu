@@ -74,4 +74,14 @@ int main() {
         sum_span += end - start;
     }
     printf("sum of spans %.1f us\n", sum_span);
+    for (int l : {8, 9, 10, 11, 20, 22}) {
+        printf("launch %d (k%d %s): blockIdx: start / stage0 / end (us from launch first start)\n", l, 3 + l / 4, nm[l % 4]);
+        double s0 = 1e30;
+        for (int c = 0; c < 512; ++c) { const unsigned long long* p = &t[((size_t)l * 512 + c) * 8]; if (p[0]) s0 = std::min(s0, (p[0] - t00) / 1e3); }
+        for (int c = 0; c < 512; c += 12) {
+            const unsigned long long* p = &t[((size_t)l * 512 + c) * 8];
+            if (!p[0]) continue;
+            printf("  %3d %6.2f %6.2f %6.2f\n", c, (p[0] - t00) / 1e3 - s0, (p[3] - t00) / 1e3 - s0, (p[5] - t00) / 1e3 - s0);
+        }
+    }
 }
