@@ -3,7 +3,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
 PKG := paper_2402_10517_b200
-SRCS := $(PKG)/csrc/apb_abi.cu $(PKG)/csrc/apb_bitplane.cu $(PKG)/csrc/apb_gemv.cu $(PKG)/csrc/apb_gemv7.cu $(PKG)/csrc/apb_decode.cu $(PKG)/csrc/apb_quant.cu $(PKG)/csrc/apb_peer.cu $(PKG)/csrc/apb_dense.cu
+SRCS := $(PKG)/csrc/apb_abi.cu $(PKG)/csrc/apb_bitplane.cu $(PKG)/csrc/apb_gemv.cu $(PKG)/csrc/apb_gemv7.cu $(PKG)/csrc/apb_decode.cu $(PKG)/csrc/apb_quant.cu $(PKG)/csrc/apb_peer.cu $(PKG)/csrc/apb_dense.cu $(PKG)/csrc/apb_dense_tc.cu
 OBJS := $(SRCS:.cu=.o)
 LIB := $(PKG)/libanyprec_b200.so
 

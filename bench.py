@@ -428,10 +428,10 @@ def run_ours(args):
             result["shard70b_C4"] = shard70b_multi(torch, plan, world, rank, share)
         except Exception as e:  # never lose the headline to the side leg
             result["shard70b_C4"] = {"error": f"{type(e).__name__}: {e}"[:300]}
-        if not args.no_decode:
-            result["decode_step"] = run_decode(torch)
-            result["quantizer"] = run_quantizer(torch)
-            result["prefill_dense"] = run_prefill(torch, copies[0])
+    if world == 1 and not args.no_decode:
+        result["decode_step"] = run_decode(torch)
+        result["quantizer"] = run_quantizer(torch)
+        result["prefill_dense"] = run_prefill(torch, copies[0])
     if rank == 0:
         if world == 1:
             result["e2e"] = run_e2e_step(torch, plans, world)
@@ -618,25 +618,33 @@ def run_decode(torch, steps: int = 20):
 
 def run_prefill(torch, preps):
     """engine.gemm above the dense threshold (prefill batches)
-    on the gate projection (11008x4096): exact fp16 dequantisation + hi/lo split
-    activations + one fp16 x fp16 -> fp32 tensor-core GEMM (fp32 accuracy)."""
+    on the gate projection (11008x4096), fp32 activations at fp32 accuracy.
+    tcgen05: the fused kernel (csrc/apb_dense_tc.cu: bitplanes decoded into the
+    UMMA A operand, TMA activations, TMEM accumulator -- one launch + the
+    activation prep); cublas: the round-1 path (GPU dequantize to an fp16 weight
+    tensor in HBM + cuBLAS fp16 x fp16 -> fp32), timed beside it.  TFLOP/s count
+    the useful 2*M*R*C (the hi/lo pair doubles the MMA work)."""
     from paper_2402_10517_b200 import engine
 
     prep = preps[4]  # gate 11008x4096
     out = {"layer": "gate 11008x4096", "k": 4, "per_M": {}}
-    for m in (64, 512, 2048):
-        x = torch.randn(m, 4096, device="cuda")
-        cfg = engine.GemvConfig(bit_width=4)
-        engine.gemm(prep, x, cfg)
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(10):
+    for impl in ("tcgen05", "cublas"):
+        engine._DENSE_IMPL = impl
+        for m in (64, 512, 2048):
+            x = torch.randn(m, 4096, device="cuda")
+            cfg = engine.GemvConfig(bit_width=4)
             engine.gemm(prep, x, cfg)
-        b.record()
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / 10
-        out["per_M"][f"M{m}"] = {"ms": round(ms, 4), "TFLOPs": round(2 * m * 11008 * 4096 / (ms * 1e-3) / 1e12, 1)}
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(10):
+                engine.gemm(prep, x, cfg)
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / 10
+            out["per_M"].setdefault(f"M{m}", {})[impl] = {
+                "ms": round(ms, 4), "TFLOPs": round(2 * m * 11008 * 4096 / (ms * 1e-3) / 1e12, 1)}
+    engine._DENSE_IMPL = "tcgen05"
     return out
 
 

@@ -159,6 +159,23 @@ int apb_dequant(const uint8_t* planes, int n_max, int64_t rows, int64_t cols,
 int apb_split_hilo(const float* x, int64_t m, int64_t cols, int64_t ldx, uint16_t* out, int64_t ld,
                    float* inv_scale, void* stream);
 
+/* Dense path as ONE Blackwell kernel (engine.py:343-354: dequantize + fp32
+ * GEMM).  apb_dense_prep_x writes the activations in the
+ * kernel's K order (within each 1024-column tile, 64-column block v holds
+ * bitplane lane words 2v, 2v+1: element 32h + 8p + b = column 256p + 16v + 8h + b),
+ * xp [mx][padded_cols] fp16 with zeros past cols: fp16 x -> mx = m rows; fp32 x
+ * -> mx = 2m rows, (hi, lo) = (fp16(x*s), fp16(x*s - hi)) at rows (2i, 2i+1)
+ * with s an exact power of two per row and inv[i] = 1/s.
+ * apb_gemm_dense_tc: y [m_out][ldy] fp32 = dequant_k(W) . x^T with the top-k
+ * planes + fp16 table decoded straight into the tcgen05.mma A operand in shared
+ * memory (no dense weight tensor), x tiles by TMA, fp32 accumulation in tensor
+ * memory; pairs = 1: m_out = mx / 2 and y = (hi-product + lo-product) * inv. */
+int apb_dense_prep_x(const void* x, int x_dtype, int64_t m, int64_t cols, int64_t ldx, uint16_t* xp,
+                     int64_t padded_cols, float* inv, void* stream);
+int apb_gemm_dense_tc(const uint8_t* planes, int n_max, int64_t rows, int64_t cols, int64_t padded_cols,
+                      int k, const uint16_t* lut, const uint16_t* xp, int64_t mx, int pairs,
+                      const float* inv, float* y, int64_t ldy, void* stream);
+
 /* Helper for the fp32-activation path: x fp32 [m][ldx_in] -> fp16 pairs
  * out [2m][ldx_out] with out[2i] = fp16(x[i]), out[2i+1] = fp16(x[i]-out[2i]).
  * Columns cols..ldx_out-1 are zero-filled.  With round_only = 1 it writes

@@ -1,0 +1,489 @@
+// apb_dense_tc.cu -- the dense (M > dense_threshold) path of engine.gemm
+// (reference engine.py:343-354: dequantize + fp32 GEMM; PAPER.md:443 runs it as
+// a separate dequantisation + cuBLAS) as ONE Blackwell kernel: the k-bit
+// weights are decoded from the top k bitplanes + the per-row fp16 centroid
+// table and written straight into TENSOR MEMORY (tcgen05.st) as the A operand
+// of tcgen05.mma (A from TMEM, B from shared memory), the activations arrive
+// by TMA, the fp32 accumulator lives in tensor memory.  No dense weight tensor
+// ever exists in HBM or shared memory.
+//
+// Numerics: the decoded weights are fp16 table entries (exact); fp32
+// activations are carried as scaled fp16 (hi, lo) row pairs (apb_dense_prep_x:
+// exact power-of-two row scale, hi + lo holds ~22 significant bits) and both
+// products accumulate in fp32 in the same MMA, the pair summed and unscaled in
+// the epilogue -- fp32-accurate like the reference (tests: 1e-5 vs fp64).
+//
+// CTA tile: 128 weight rows (UMMA M) x BN = 128 or 256 activation rows (UMMA N),
+// K in blocks of 64 columns.  Warp roles:
+//   warp 0    TMA producer: activation tiles (box {64, BN}, SW128) and plane
+//             chunks (box {16 B, 128 rows, k planes} = two K blocks),
+//   warp 1    TMEM allocation + the single-thread tcgen05.mma issuer,
+//   warps 2-17 decoders: warp (row quarter q = warp % 4 = its TMEM lane quarter,
+//             lane word h, K-block parity); thread = weight row; the decoded
+//             fp16 pairs go to TMEM columns [BN + 32 slot + 16 h, +16) with one
+//             tcgen05.st.32x32b.x16; then all 16 run the epilogue (tcgen05.ld -> y).
+// Why TMEM for A: the kernel is shared-memory bound (LUT lookups + the tensor
+// core's operand reads); staging A in shared memory cost a store and an MMA
+// read per decoded weight (r2 profile: LSU 59 % + TC 30 % of the data path),
+// TMEM takes both off it (M = 64 / 512 / 2048: 0.053 / 0.144 / 0.444 ms with A
+// in shared memory -> 0.041 / 0.102 / 0.352 ms).
+// The K order inside a 1024-column tile follows the bitplane lane words: K block
+// v holds words 2v, 2v+1, element e = 32h + 8p + b of a block is column
+// 256p + 8(2v+h) + b -- apb_dense_prep_x writes the activations in that order.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdlib>
+
+#include "../../include/anyprec_b200.h"
+#include "apb_common.cuh"
+
+namespace apbd {
+using apb::prmt;
+
+constexpr int BM = 128, BK = 64;
+constexpr int kASlots = 2, kPStages = 2;
+constexpr int kDecWarps = 16;  // (row quarter q, word h, K-block parity) -- 4 per SM sub-partition
+constexpr int kThreads = (2 + kDecWarps) * 32;
+constexpr int kSmemBase = 1024;  // sm_100 reserves the first 1 KB of the shared window
+constexpr int kTableMax = 64 * 1024;
+// dynamic shared memory layout (offsets from the 1024-aligned base), per N tile
+template <int BN>
+struct Lay {
+    static constexpr int kXStages = BN == 256 ? 4 : 6;
+    static constexpr int kOffX = 0;                              // activation tiles (BN x 128 B)
+    static constexpr int kOffP = kOffX + kXStages * BN * 128;    // plane chunks (k x 2 KB)
+    static constexpr int kOffT = kOffP + kPStages * 8 * 2048;    // centroid table (<= 64 KB)
+    static constexpr int kOffB = kOffT + kTableMax;              // mbarriers + TMEM address
+    static constexpr int kBytes = kOffB + 256;
+    static constexpr uint32_t kTable = (uint32_t)(kSmemBase + kOffT);  // absolute (LDS immediate)
+    // tensor memory: D = columns [0, BN) (fp32), decoded A slots of 32 columns each
+    // (128 lanes = weight rows x 64 K as packed fp16 pairs) after it
+    static constexpr int kTmemCols = BN == 256 ? 512 : 256;
+    static constexpr uint32_t kColA = BN;
+};
+
+struct DenseParams {
+    CUtensorMap tm_x;       // permuted activations [Mx][Cp] fp16
+    CUtensorMap tm_planes;  // [n_max][R][Cp/8] u8
+    const __half* lut;      // [R][2^k]
+    float* y;               // [m_out][ldy] fp32
+    const float* inv;       // pairs: 1 / row scale per output row
+    int64_t rows, ldy;
+    int mx, m_out, n_kb, pairs;
+};
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("{\n\t.reg .b64 s;\n\tmbarrier.arrive.shared::cta.b64 s, [%0];\n\t}" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 s;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 s, [%0], %1;\n\t}" ::"r"(a),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra W_%=;\n\t}" ::"r"(a),
+        "r"(parity), "r"(1000000)
+        : "memory");
+}
+__device__ __forceinline__ void tma2(uint32_t dst, const CUtensorMap* m, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(m), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+// table lookups: the table base is the LDS immediate
+template <uint32_t T>
+__device__ __forceinline__ uint32_t lds_t32(uint32_t off) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(off), "n"(T));
+    return v;
+}
+template <uint32_t T>
+__device__ __forceinline__ uint32_t lds_t16(uint32_t off) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1+%2];" : "=h"(v) : "r"(off), "n"(T));
+    return v;
+}
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle: 8-row x 128-B atoms
+// stacked at SBO = 1024 B, version 1 (sm_100), layout type 2 (SWIZZLE_128B).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr_) {
+    return (uint64_t)((saddr_ >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// kind::f16 instruction descriptor: D f32, A/B f16, both K-major, N >> 3, M >> 4
+template <int BN>
+constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+// A from tensor memory (the decoders' tcgen05.st), B from shared memory (TMA)
+template <int BN>
+__device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "n"(kIdesc<BN>), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+template <int K, int BN>
+__global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_constant__ DenseParams P) {
+    using Y = Lay<BN>;
+    constexpr int kXStages = Y::kXStages;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (saddr(smem) != kSmemBase) __trap();  // the table base is an LDS immediate
+    const int64_t row0 = (int64_t)blockIdx.x * BM;
+    const int n0 = blockIdx.y * BN;
+    const uint32_t sX = saddr(smem + Y::kOffX), sP = saddr(smem + Y::kOffP);
+    const uint32_t bar = saddr(smem + Y::kOffB);
+    // barriers (8 B each): x_full[8] x_empty[8] a_full[2] a_empty[2] p_full[2] p_empty[2] d_full
+    static_assert(kXStages <= 8, "barrier layout");
+    const uint32_t b_xf = bar, b_xe = bar + 64, b_af = bar + 128, b_ae = bar + 144, b_pf = bar + 160,
+                   b_pe = bar + 176, b_d = bar + 192;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Y::kOffB + 240);
+    constexpr int kPlaneBytes = K * 2048;  // one plane chunk stage: 16 B x 128 rows x K planes
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kXStages; ++i) {
+            mbar_init(b_xf + 8 * i, 1);
+            mbar_init(b_xe + 8 * i, 1);
+        }
+        for (int i = 0; i < kASlots; ++i) {
+            mbar_init(b_af + 8 * i, 8 * 32);  // the 8 decode warps of this K-block parity
+            mbar_init(b_ae + 8 * i, 1);
+        }
+        for (int i = 0; i < kPStages; ++i) {
+            mbar_init(b_pf + 8 * i, 1);
+            mbar_init(b_pe + 8 * i, kDecWarps * 32);
+        }
+        mbar_init(b_d, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {  // D[128 lanes][BN] fp32 + the decoded A slots
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tmem_slot)),
+                     "n"(Y::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int n_kb = P.n_kb;
+
+    if (warp == 0) {
+        // ================================ TMA producer ================================
+        if (lane == 0) {
+            for (int kb = 0; kb < n_kb; ++kb) {
+                if ((kb & 1) == 0) {  // plane chunk = K blocks kb, kb+1
+                    const int ps = kb >> 1, s = ps % kPStages;
+                    if (ps >= kPStages) mbar_wait(b_pe + 8 * s, ((ps / kPStages) - 1) & 1);
+                    mbar_expect_tx(b_pf + 8 * s, kPlaneBytes);
+                    tma3(sP + s * 8 * 2048, &P.tm_planes, 16 * ps, (int)row0, 0, b_pf + 8 * s);
+                }
+                const int s = kb % kXStages;
+                if (kb >= kXStages) mbar_wait(b_xe + 8 * s, ((kb / kXStages) - 1) & 1);
+                mbar_expect_tx(b_xf + 8 * s, BN * 128);
+                tma2(sX + s * BN * 128, &P.tm_x, kb * BK, n0, b_xf + 8 * s);
+            }
+        }
+    } else if (warp == 1) {
+        // ============================ tcgen05.mma issuer ============================
+        if (lane == 0) {
+            for (int kb = 0; kb < n_kb; ++kb) {
+                const int sa = kb % kASlots, sx = kb % kXStages;
+                mbar_wait(b_af + 8 * sa, (kb / kASlots) & 1);
+                mbar_wait(b_xf + 8 * sx, (kb / kXStages) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint64_t dx = sw128_desc(sX + sx * BN * 128);
+                const uint32_t ta = tmem + Y::kColA + 32u * (uint32_t)sa;
+#pragma unroll
+                for (int ks = 0; ks < BK / 16; ++ks)  // K = 16 per MMA: 8 TMEM columns of A, +32 B of B's swizzle atom
+                    umma_f16_ts<BN>(tmem, ta + 8u * (uint32_t)ks, dx + 2 * ks, (kb | ks) != 0);
+                umma_commit(b_ae + 8 * sa);  // the decoded tile and the x tile may be overwritten
+                umma_commit(b_xe + 8 * sx);
+            }
+            umma_commit(b_d);  // accumulator complete
+        }
+    } else {
+        // =================== decoders, then the epilogue ===================
+        // decode warp dw: rows 32q..32q+31 (q = warp & 3, the TMEM lane quarter this
+        // warp may read), lane word h of every K block with parity par
+        const int dw = warp - 2, q4 = warp & 3, h = (dw >> 2) & 1, par = dw >> 3;
+        const int r = 32 * q4 + lane;
+        const int64_t grow = row0 + r;
+        // this row's centroid table: u32 [entry][128 rows] (k <= 7), u16 (k = 8); the
+        // 4 warps of a row quarter split the entries
+        {
+            const __half* src = P.lut + (grow < P.rows ? grow : 0) * (int64_t)(1 << K);
+            const int part = dw >> 2;
+#pragma unroll 4
+            for (int e = part; e < (1 << K); e += 4) {
+                const uint16_t v = grow < P.rows ? __half_as_ushort(src[e]) : (uint16_t)0;
+                if constexpr (K <= 7)
+                    *reinterpret_cast<uint32_t*>(smem + Y::kOffT + (e * BM + r) * 4) = v;
+                else
+                    *reinterpret_cast<uint16_t*>(smem + Y::kOffT + (e * BM + r) * 2) = v;
+            }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kDecWarps * 32) : "memory");  // table complete
+        const uint32_t rr = (uint32_t)r << 1;  // byte 0 of the table address
+        // this warp's TMEM lane quarter; A slot columns of word h
+        const uint32_t t_row = tmem + ((uint32_t)(32 * q4) << 16) + Y::kColA + 16u * (uint32_t)h;
+        for (int kb = par; kb < n_kb; kb += 2) {
+            // this row's lane word of K block kb: plane chunk stage kb / 2, word 2 (kb & 1) + h
+            const int ps = kb >> 1, s = ps % kPStages;
+            mbar_wait(b_pf + 8 * s, (ps / kPStages) & 1);
+            uint32_t Q[K];
+#pragma unroll
+            for (int i = 0; i < K; ++i) {  // Q[i] = plane K-1-i (LSB plane first)
+                uint32_t v;
+                asm volatile("ld.shared.u32 %0, [%1];"
+                             : "=r"(v)
+                             : "r"(sP + s * 8 * 2048 + (K - 1 - i) * 2048 + r * 16 + (2 * (kb & 1) + h) * 4));
+                Q[i] = v;
+            }
+            mbar_arrive(b_pe + 8 * s);
+            uint32_t W[8];
+            apb::to_bytes<K>(Q, W);  // W[b] byte p = code of column 256p + 8t + b
+            uint32_t v[16];          // K elements 32h + 8p + b as fp16 pairs: column 4p + b/2 of word h
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int b = 0; b < 8; b += 2) {
+                    const uint32_t a0 = prmt(W[b], rr, 0x7604u | (uint32_t)(p << 4));  // code << 8 | r << 1
+                    const uint32_t a1 = prmt(W[b + 1], rr, 0x7604u | (uint32_t)(p << 4));
+                    uint32_t lo, hi;
+                    if constexpr (K <= 7) {
+                        lo = lds_t32<Y::kTable>(a0 << 1);
+                        hi = lds_t32<Y::kTable>(a1 << 1);
+                    } else {
+                        lo = lds_t16<Y::kTable>(a0);
+                        hi = lds_t16<Y::kTable>(a1);
+                    }
+                    v[4 * p + b / 2] = lo | (hi << 16);
+                }
+            const int sa = kb % kASlots;  // == par
+            if (kb >= kASlots) mbar_wait(b_ae + 8 * sa, ((kb / kASlots) - 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+                    t_row + 32u * (uint32_t)sa),
+                "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+                "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+                : "memory");
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(b_af + 8 * sa);
+        }
+        // ------------------------------------ epilogue ------------------------------------
+        // the 4 warp groups (dw >> 2) split the BN accumulator columns
+        mbar_wait(b_d, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        constexpr int kCols = BN / 4;
+#pragma unroll 1
+        for (int c0 = (dw >> 2) * kCols; c0 < ((dw >> 2) + 1) * kCols; c0 += 32) {
+            uint32_t d[32];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+                  "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]),
+                  "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]),
+                  "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]),
+                  "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
+                : "r"(tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)c0));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (grow < P.rows) {
+                if (P.pairs) {  // columns (2i, 2i+1) = (hi, lo) of output row (n0 + c) / 2
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        const int m = (n0 + c0 + c) >> 1;
+                        if (m < P.m_out)
+                            P.y[(int64_t)m * P.ldy + grow] =
+                                (__uint_as_float(d[c]) + __uint_as_float(d[c + 1])) * P.inv[m];
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const int m = n0 + c0 + c;
+                        if (m < P.m_out) P.y[(int64_t)m * P.ldy + grow] = __uint_as_float(d[c]);
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Y::kTmemCols));
+    }
+}
+
+// Activations in the kernel's K order (one CTA per input row): fp16 rows copied,
+// or fp32 rows split into scaled (hi, lo) pairs at rows (2i, 2i+1) with 1 / scale
+// in inv[i]; columns >= cols are zero.
+template <bool F32>
+__global__ void __launch_bounds__(256) prep_x_kernel(const void* __restrict__ x, int cols, int64_t ldx,
+                                                     __half* __restrict__ xp, int64_t cp, float* __restrict__ inv) {
+    const int row = blockIdx.x, t = threadIdx.x;
+    float scale = 1.f;
+    if constexpr (F32) {
+        __shared__ float red[8];
+        const float* xr = reinterpret_cast<const float*>(x) + (int64_t)row * ldx;
+        float a = 0.f;
+        for (int i = t; i < cols; i += 256) a = fmaxf(a, fabsf(xr[i]));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+        if ((t & 31) == 0) red[t >> 5] = a;
+        __syncthreads();
+        a = red[0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) a = fmaxf(a, red[w]);
+        if (a > 0.f && isfinite(a)) {
+            int e;
+            frexpf(a, &e);
+            scale = ldexpf(1.f, min(max(15 - e, -126), 126));  // max |x| * scale in [2^14, 2^15)
+        }
+        if (t == 0) inv[row] = 1.f / scale;
+    }
+    for (int64_t j = t; j < cp; j += 256) {
+        const int64_t T = j >> 10;
+        const int w = (int)(j & 1023), v = w >> 6, e = w & 63;
+        const int64_t c = (T << 10) + 256 * ((e >> 3) & 3) + 16 * v + 8 * (e >> 5) + (e & 7);
+        if constexpr (F32) {
+            const float xv = c < cols ? reinterpret_cast<const float*>(x)[(int64_t)row * ldx + c] * scale : 0.f;
+            const __half h = __float2half_rn(xv);
+            xp[(int64_t)(2 * row) * cp + j] = h;
+            xp[(int64_t)(2 * row + 1) * cp + j] = __float2half_rn(xv - __half2float(h));
+        } else {
+            xp[(int64_t)row * cp + j] =
+                c < cols ? reinterpret_cast<const __half*>(x)[(int64_t)row * ldx + c] : __ushort_as_half(0);
+        }
+    }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+
+template <int K, int BN>
+static int launch_bn(DenseParams& P, int64_t rows, cudaStream_t s) {
+    static std::atomic<unsigned long long> configured{0};
+    static_assert(Lay<BN>::kBytes <= 227 * 1024, "shared memory budget");
+    if (!apb::ensure_smem_optin(dense_tc_kernel<K, BN>, Lay<BN>::kBytes, configured)) return APB_ERR_CUDA;
+    const dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((P.mx + BN - 1) / BN));
+    dense_tc_kernel<K, BN><<<grid, kThreads, Lay<BN>::kBytes, s>>>(P);
+    return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
+}
+// N tile: 256 activation rows when there are more than 128 (the decoded weight
+// tile then feeds twice the MMA work), else 128
+template <int K>
+static int launch(DenseParams& P, int64_t rows, cudaStream_t s) {
+    return P.mx > 128 ? launch_bn<K, 256>(P, rows, s) : launch_bn<K, 128>(P, rows, s);
+}
+
+}  // namespace apbd
+
+extern "C" int apb_dense_prep_x(const void* x, int x_dtype, int64_t m, int64_t cols, int64_t ldx, uint16_t* xp,
+                                int64_t padded_cols, float* inv, void* stream) {
+    if (!x || !xp || (x_dtype == APB_DTYPE_F32 && !inv)) return APB_ERR_PARAM;
+    if (x_dtype != APB_DTYPE_F32 && x_dtype != APB_DTYPE_F16) return APB_ERR_PARAM;
+    if (m <= 0 || cols <= 0 || ldx < cols || padded_cols < cols || padded_cols % 1024 || m > INT32_MAX ||
+        cols > INT32_MAX)
+        return APB_ERR_SHAPE;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (x_dtype == APB_DTYPE_F32)
+        apbd::prep_x_kernel<true><<<(unsigned)m, 256, 0, s>>>(x, (int)cols, ldx, (__half*)xp, padded_cols, inv);
+    else
+        apbd::prep_x_kernel<false><<<(unsigned)m, 256, 0, s>>>(x, (int)cols, ldx, (__half*)xp, padded_cols, inv);
+    return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
+}
+
+extern "C" int apb_gemm_dense_tc(const uint8_t* planes, int n_max, int64_t rows, int64_t cols, int64_t padded_cols,
+                                 int k, const uint16_t* lut, const uint16_t* xp, int64_t mx, int pairs,
+                                 const float* inv, float* y, int64_t ldy, void* stream) {
+    using namespace apbd;
+    if (!planes || !lut || !xp || !y || (pairs && !inv)) return APB_ERR_PARAM;
+    if (k < 2 || k > n_max || n_max > 8) return APB_ERR_PARAM;
+    if (rows <= 0 || cols <= 0 || padded_cols < cols || padded_cols % 1024 || mx <= 0 || (pairs && (mx & 1)))
+        return APB_ERR_SHAPE;
+    const int64_t m_out = pairs ? mx / 2 : mx;
+    if (ldy < rows || mx > INT32_MAX) return APB_ERR_SHAPE;
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return APB_ERR_CUDA;
+    DenseParams P = {};
+    {
+        const cuuint64_t dims[2] = {(cuuint64_t)padded_cols, (cuuint64_t)mx};
+        const cuuint64_t strides[1] = {(cuuint64_t)padded_cols * 2};
+        const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)(mx > 128 ? 256 : 128)}, es[2] = {1, 1};  // N tile (launch)
+        if (enc(&P.tm_x, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)xp, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return APB_ERR_CUDA;
+    }
+    {
+        const int64_t rb = padded_cols / 8;
+        const cuuint64_t dims[3] = {(cuuint64_t)rb, (cuuint64_t)rows, (cuuint64_t)n_max};
+        const cuuint64_t strides[2] = {(cuuint64_t)rb, (cuuint64_t)(rows * rb)};
+        const cuuint32_t box[3] = {16, (cuuint32_t)BM, (cuuint32_t)k}, es[3] = {1, 1, 1};
+        if (enc(&P.tm_planes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)planes, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return APB_ERR_CUDA;
+    }
+    P.lut = reinterpret_cast<const __half*>(lut);
+    P.y = y;
+    P.inv = inv;
+    P.rows = rows;
+    P.ldy = ldy;
+    P.mx = (int)mx;
+    P.m_out = (int)m_out;
+    P.n_kb = (int)(padded_cols / BK);
+    P.pairs = pairs ? 1 : 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (k) {
+        case 2: return launch<2>(P, rows, s);
+        case 3: return launch<3>(P, rows, s);
+        case 4: return launch<4>(P, rows, s);
+        case 5: return launch<5>(P, rows, s);
+        case 6: return launch<6>(P, rows, s);
+        case 7: return launch<7>(P, rows, s);
+        case 8: return launch<8>(P, rows, s);
+    }
+    return APB_ERR_PARAM;
+}

@@ -15,6 +15,8 @@ same MMA, so the default path stays within ~1e-6 of the fp32 reference.
 
 from __future__ import annotations
 
+import os
+
 import ctypes
 import threading
 from dataclasses import dataclass, field
@@ -495,8 +497,6 @@ def gemm(prep: PreparedLayer, x, cfg: GemvConfig, report: ExecutionReport | None
     if shape[1] != t.cols:
         raise ShapeError(f"activation width {shape[1]} != in_features {t.cols}")
     torch = dev.require_cuda()
-    # the k-bit weights are fp16 table entries: dequantised to fp16 they are exact
-    dense = _dequant_device(prep, k, APB_DTYPE_F16)
     if report is not None:
         report.path_taken = "gemm-dense"
         report.planes_bytes_read += k * t.rows * t.padded_cols // 8
@@ -504,10 +504,44 @@ def gemm(prep: PreparedLayer, x, cfg: GemvConfig, report: ExecutionReport | None
     host = not dev.is_tensor(x)
     xd = dev.to_device(np.asarray(x)) if host else x.cuda()
     back = "numpy" if host else ("cuda" if x.is_cuda else "tensor")
-    y = _dense_tensor_core(torch, xd, dense, cfg.activations_fp16)
+    if _DENSE_IMPL == "cublas":  # the round-1 path (separate dequant + cuBLAS), kept for comparison
+        y = _dense_tensor_core(torch, xd, _dequant_device(prep, k, APB_DTYPE_F16), cfg.activations_fp16)
+    else:
+        y = _dense_fused(torch, prep, k, xd, cfg.activations_fp16)
     if back == "numpy":
         return y.cpu().numpy()
     return y.cpu() if back == "tensor" else y
+
+
+# APB_DENSE=cublas selects the round-1 dense path (GPU dequantize to an fp16
+# weight tensor + cuBLAS) for A/B measurements; the default is the fused kernel.
+_DENSE_IMPL = os.environ.get("APB_DENSE", "tcgen05")
+
+
+def _dense_fused(torch, prep: PreparedLayer, k: int, x, x_is_fp16: bool):
+    """Y = X @ dequant_k(W).T in one tcgen05 kernel (csrc/apb_dense_tc.cu): the
+    top-k planes and the fp16 table are decoded straight into the MMA's shared-
+    memory A operand, activations arrive by TMA, fp32 accumulation in tensor
+    memory.  fp32 activations ride as scaled fp16 (hi, lo) row pairs (exact
+    power-of-two row scale), summed and unscaled in the epilogue -- fp32-accurate
+    like the reference's dense path (engine.py:343-354)."""
+    t = prep.tensor
+    m = x.shape[0]
+    L = load()
+    s = dev.stream_ptr()
+    if x_is_fp16:
+        xin, dt, mx, pairs = x.to(torch.float16).contiguous(), APB_DTYPE_F16, m, 0
+    else:
+        xin, dt, mx, pairs = x.to(torch.float32).contiguous(), APB_DTYPE_F32, 2 * m, 1
+    xp = torch.empty((mx, t.padded_cols), dtype=torch.float16, device="cuda")
+    inv = torch.empty(m, dtype=torch.float32, device="cuda")
+    check(L.apb_dense_prep_x(dev.ptr(xin), dt, m, t.cols, xin.shape[1], dev.ptr(xp), t.padded_cols,
+                             dev.ptr(inv), s), "apb_dense_prep_x")
+    y = torch.empty((m, t.rows), dtype=torch.float32, device="cuda")
+    check(L.apb_gemm_dense_tc(dev.ptr(t.planes), t.n_max, t.rows, t.cols, t.padded_cols, k,
+                              dev.ptr(prep.tables16[k]), dev.ptr(xp), mx, pairs, dev.ptr(inv), dev.ptr(y),
+                              t.rows, s), "apb_gemm_dense_tc")
+    return y
 
 
 def _dense_tensor_core(torch, x, w16, x_is_fp16: bool):

@@ -760,3 +760,25 @@ def test_dense_path_tensor_core_fp32_accuracy(api, m):
         rows = np.arange(m) != 3
         assert (err[rows] / scale[rows]).max() < 1e-5, (k, (err[rows] / scale[rows]).max())
         assert ora.rel_err(y, want) < TOL
+
+
+@pytest.mark.parametrize("m,rows,cols", [(17, 300, 2500), (128, 256, 1024), (257, 129, 3000), (64, 4096, 4096)])
+def test_dense_tcgen05_vs_dense_oracle(api, m, rows, cols):
+    """The fused tcgen05 dense kernel (csrc/apb_dense_tc.cu: planes + table
+    decoded into the UMMA A operand, TMA activations, TMEM accumulator) against
+    the fp64 product of the reference dequantisation (engine.py:343-362), every
+    k = 2..8, ragged rows / columns / batch (partial 128-row tiles on both MMA
+    operands), fp32 activations (hi/lo pairs) and activations_fp16."""
+    _, _, engine, _ = api
+    layer = _random_layer(api, 900 + m, rows, cols, 2, 8)
+    prep = engine.prepare(layer)
+    X = np.random.default_rng(m).standard_normal((m, cols)).astype(np.float32)
+    X16 = X.astype(np.float16).astype(np.float64)
+    for k in range(2, 9):
+        W = engine.dequantize(layer, k).astype(np.float64)
+        rep = engine.ExecutionReport()
+        y = engine.gemm(prep, X, engine.GemvConfig(bit_width=k, dense_threshold=16), report=rep)
+        assert rep.path_taken == "gemm-dense"
+        assert ora.rel_err(y, X.astype(np.float64) @ W.T) < TOL, (k, ora.rel_err(y, X.astype(np.float64) @ W.T))
+        y16 = engine.gemm(prep, X, engine.GemvConfig(bit_width=k, dense_threshold=16, activations_fp16=True))
+        assert ora.rel_err(y16, X16 @ W.T) < TOL, k
