@@ -6,7 +6,7 @@ cd "$(dirname "$0")/../.."
 while [ $# -ge 2 ]; do
   d=tools/kbench/var_$1; mkdir -p $d
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared $2 \
-     -o $d/libanyprec_b200.so paper_2402_10517_b200/csrc/apb_abi.cu paper_2402_10517_b200/csrc/apb_bitplane.cu paper_2402_10517_b200/csrc/apb_gemv.cu paper_2402_10517_b200/csrc/apb_gemv7.cu paper_2402_10517_b200/csrc/apb_decode.cu paper_2402_10517_b200/csrc/apb_quant.cu paper_2402_10517_b200/csrc/apb_peer.cu paper_2402_10517_b200/csrc/apb_dense.cu &
+     -o $d/libanyprec_b200.so paper_2402_10517_b200/csrc/*.cu &
   shift 2
 done
 wait
