@@ -942,6 +942,42 @@ def cpu_baseline():
             "seconds": round(dt * steps, 2), "cpu_model": _cpu_model()}
 
 
+def _stock_reference_sample():
+    """The UNMODIFIED reference package (pip-installed offline from /root/reference
+    into baseline/_ref, git-ignored, travels with the snapshot) timed through its
+    own public API: anyprec.engine.prepare + engine.gemv (numpy, one host thread)
+    on BASELINE configs[0] -- one 4096x4096 layer at k = 3..8 -- as a second CPU
+    data point beside the C port.  Algorithmic bytes as everywhere."""
+    ref_root = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_root, "anyprec")):
+        return {"unavailable": "baseline/_ref not installed"}
+    import importlib
+
+    sys.path.insert(0, ref_root)
+    try:
+        E = importlib.import_module("anyprec.engine")
+        Q = importlib.import_module("anyprec.quantizer")
+        from oracle import oracle as ora
+
+        rows = cols = 4096
+        codes, tables = ora.random_layer_arrays(np.random.default_rng(0), rows, cols, 3, N_MAX)
+        layer = Q.AnyPrecisionLayer(n_min=3, n_max=N_MAX, codes=codes, centroid_tables=tables, shape=(rows, cols))
+        prep = E.prepare(layer)
+        x = np.random.default_rng(1).standard_normal(cols)
+        t0 = time.perf_counter()
+        for k in BITS:
+            E.gemv(prep, x, E.GemvConfig(bit_width=k))
+        dt = time.perf_counter() - t0
+        alg = sum(alg_bytes(rows, cols, k) for k in BITS)
+        return {"value": round(alg / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "reference",
+                "seconds": round(dt, 2), "sample": "anyprec.engine.gemv (unmodified reference, numpy) on one "
+                "4096x4096 layer (configs[0]) at k = 3..8, one call each"}
+    except Exception as e:  # never lose the reference line to the side leg
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+    finally:
+        sys.path.remove(ref_root)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -966,6 +1002,7 @@ def run_reference(args):
                          "sample": f"{steps} full step(s), {threads} threads, oracle/anyprec_oracle.c "
                                    "(C port of the reference engine.py pipeline)", "cpu_model": _cpu_model()},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "stock_reference_python": _stock_reference_sample(),
     }))
 
 

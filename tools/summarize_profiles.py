@@ -82,4 +82,4 @@ for d in data:
     rd *= scale.get(u[h.index("dram__bytes_read.sum")], 1); wr *= scale.get(u[h.index("dram__bytes_write.sum")], 1)
     tr.append({"kernel": name.split("(")[0].replace("void ", ""), "dram_bytes": rd + wr})
 json.dump({"source": f"profiles/{tag}_ncu_full.md (ncu --set full)", "launches": tr},
-          open(os.path.join(ROOT, "profiles", f"{tag}_traffic.json"), "w"), indent=1)
+          open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full_traffic.json"), "w"), indent=1)
