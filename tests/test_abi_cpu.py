@@ -79,6 +79,19 @@ def test_host_validation_before_launch(lib):
     assert lib.apb_permute(fake, fake, 1, 1, 1024, 0, nul) == 2
     # dequant dtype
     assert lib.apb_dequant(fake, 8, 4, 1024, 1024, 1, 3, fake, fake, 7, 1024, nul) == 2
+    # fused tcgen05 dense path (engine.py:343-354): activation prep and GEMM validate first
+    F32, F16 = 0, 1
+    assert lib.apb_dense_prep_x(fake, F32, 4, 1000, 1000, fake, 1000, fake, nul) == 1  # padded % 1024
+    assert lib.apb_dense_prep_x(fake, F32, 4, 1000, 999, fake, 1024, fake, nul) == 1   # ldx < cols
+    assert lib.apb_dense_prep_x(fake, F32, 4, 1000, 1000, fake, 1024, nul, nul) == 2   # fp32 needs inv
+    assert lib.apb_dense_prep_x(fake, 7, 4, 1000, 1000, fake, 1024, fake, nul) == 2    # dtype
+    assert lib.apb_dense_prep_x(fake, F16, 0, 1000, 1000, fake, 1024, nul, nul) == 1   # empty batch
+    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 9, fake, fake, 64, 1, fake, fake, 16, nul) == 2  # k
+    assert lib.apb_gemm_dense_tc(fake, 4, 16, 1024, 1024, 5, fake, fake, 64, 1, fake, fake, 16, nul) == 2  # k > n_max
+    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1000, 4, fake, fake, 64, 1, fake, fake, 16, nul) == 1  # padded
+    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 63, 1, fake, fake, 16, nul) == 1  # odd pairs
+    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 64, 1, nul, fake, 16, nul) == 2  # pairs need inv
+    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 64, 0, nul, fake, 8, nul) == 1   # ldy < rows
 
 
 def test_status_mapping():
