@@ -174,7 +174,12 @@ int apb_dense_prep_x(const void* x, int x_dtype, int64_t m, int64_t cols, int64_
                      int64_t padded_cols, float* inv, void* stream);
 int apb_gemm_dense_tc(const uint8_t* planes, int n_max, int64_t rows, int64_t cols, int64_t padded_cols,
                       int k, const uint16_t* lut, const uint16_t* xp, int64_t mx, int pairs,
-                      const float* inv, float* y, int64_t ldy, void* stream);
+                      const float* inv, float* y, int64_t ldy, float* ws, int64_t ws_bytes, void* stream);
+/* Workspace bytes apb_gemm_dense_tc uses for split-K on this device (0: none):
+ * when the output tiles cannot cover the SMs (small batch), K is split into
+ * 2..8 chunks whose fp32 partial tiles are summed in fixed order by a second
+ * kernel (deterministic).  ws = NULL / too small -> a single pass. */
+int64_t apb_gemm_dense_tc_workspace(int64_t rows, int64_t padded_cols, int64_t mx);
 
 /* Helper for the fp32-activation path: x fp32 [m][ldx_in] -> fp16 pairs
  * out [2m][ldx_out] with out[2i] = fp16(x[i]), out[2i+1] = fp16(x[i]-out[2i]).

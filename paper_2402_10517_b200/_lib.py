@@ -98,7 +98,8 @@ SIGNATURES = {
     "apb_peer_handle_bytes": ([], _I),
     "apb_split_hilo": ([_P, _I64, _I64, _I64, _P, _I64, _P, _P], _I),
     "apb_dense_prep_x": ([_P, _I, _I64, _I64, _I64, _P, _I64, _P, _P], _I),
-    "apb_gemm_dense_tc": ([_P, _I, _I64, _I64, _I64, _I, _P, _P, _I64, _I, _P, _P, _I64, _P], _I),
+    "apb_gemm_dense_tc": ([_P, _I, _I64, _I64, _I64, _I, _P, _P, _I64, _I, _P, _P, _I64, _P, _I64, _P], _I),
+    "apb_gemm_dense_tc_workspace": ([_I64, _I64, _I64], _I64),
     "apb_quant_workspace": ([_I, _I, _I, _I], _I64),
     "apb_quant_build": ([_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I64, _P], _I),
     "apb_quant_continue": ([_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I64, _P], _I),

@@ -72,8 +72,10 @@ struct DenseParams {
     const __half* lut;      // [R][2^k]
     float* y;               // [m_out][ldy] fp32
     const float* inv;       // pairs: 1 / row scale per output row
+    float* ws;              // split-K: raw fp32 accumulator tiles [splits][mx][rows]
     int64_t rows, ldy;
-    int mx, m_out, n_kb, pairs;
+    int mx, m_out, n_kb, pairs;  // n_kb: K blocks per split (even)
+    int splits;
 };
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -191,7 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    const int n_kb = P.n_kb;
+    const int n_kb = P.n_kb;                  // this CTA's K blocks (split-K: blockIdx.z's share)
+    const int kb0 = (int)blockIdx.z * n_kb;  // first global K block (even)
 
     if (warp == 0) {
         // ================================ TMA producer ================================
@@ -201,12 +204,12 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
                     const int ps = kb >> 1, s = ps % kPStages;
                     if (ps >= kPStages) mbar_wait(b_pe + 8 * s, ((ps / kPStages) - 1) & 1);
                     mbar_expect_tx(b_pf + 8 * s, kPlaneBytes);
-                    tma3(sP + s * 8 * 2048, &P.tm_planes, 16 * ps, (int)row0, 0, b_pf + 8 * s);
+                    tma3(sP + s * 8 * 2048, &P.tm_planes, 16 * ((kb0 >> 1) + ps), (int)row0, 0, b_pf + 8 * s);
                 }
                 const int s = kb % kXStages;
                 if (kb >= kXStages) mbar_wait(b_xe + 8 * s, ((kb / kXStages) - 1) & 1);
                 mbar_expect_tx(b_xf + 8 * s, BN * 128);
-                tma2(sX + s * BN * 128, &P.tm_x, kb * BK, n0, b_xf + 8 * s);
+                tma2(sX + s * BN * 128, &P.tm_x, (kb0 + kb) * BK, n0, b_xf + 8 * s);
             }
         }
     } else if (warp == 1) {
@@ -316,7 +319,13 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
                   "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
                 : "r"(tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)c0));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (grow < P.rows) {
+            if (grow < P.rows && P.splits > 1) {  // split-K: raw partial tile, summed by split_sum_kernel
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const int n = n0 + c0 + c;
+                    if (n < P.mx) P.ws[((int64_t)blockIdx.z * P.mx + n) * P.rows + grow] = __uint_as_float(d[c]);
+                }
+            } else if (grow < P.rows) {
                 if (P.pairs) {  // columns (2i, 2i+1) = (hi, lo) of output row (n0 + c) / 2
 #pragma unroll
                     for (int c = 0; c < 32; c += 2) {
@@ -386,6 +395,23 @@ __global__ void __launch_bounds__(256) prep_x_kernel(const void* __restrict__ x,
     }
 }
 
+// split-K epilogue: y = sum over splits (fixed order: deterministic) of the raw
+// accumulator tiles, (hi, lo) columns added and unscaled for pairs.
+__global__ void __launch_bounds__(256) split_sum_kernel(const float* __restrict__ ws, int splits, int mx, int64_t rows,
+                                                        int pairs, const float* __restrict__ inv, float* __restrict__ y,
+                                                        int64_t ldy, int m_out) {
+    const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (i >= (int64_t)m_out * rows) return;
+    const int m = (int)(i / rows);
+    const int64_t r = i - (int64_t)m * rows;
+    float acc = 0.f;
+    for (int z = 0; z < splits; ++z) {
+        const float* t = ws + (int64_t)z * mx * rows;
+        acc += pairs ? t[(int64_t)(2 * m) * rows + r] + t[(int64_t)(2 * m + 1) * rows + r] : t[(int64_t)m * rows + r];
+    }
+    y[(int64_t)m * ldy + r] = pairs ? acc * inv[m] : acc;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -406,8 +432,14 @@ static int launch_bn(DenseParams& P, int64_t rows, cudaStream_t s) {
     static std::atomic<unsigned long long> configured{0};
     static_assert(Lay<BN>::kBytes <= 227 * 1024, "shared memory budget");
     if (!apb::ensure_smem_optin(dense_tc_kernel<K, BN>, Lay<BN>::kBytes, configured)) return APB_ERR_CUDA;
-    const dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((P.mx + BN - 1) / BN));
+    const dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((P.mx + BN - 1) / BN), (unsigned)P.splits);
     dense_tc_kernel<K, BN><<<grid, kThreads, Lay<BN>::kBytes, s>>>(P);
+    if (cudaGetLastError() != cudaSuccess) return APB_ERR_CUDA;
+    if (P.splits > 1) {
+        const int64_t n = (int64_t)P.m_out * rows;
+        split_sum_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P.ws, P.splits, P.mx, rows, P.pairs, P.inv, P.y,
+                                                                     P.ldy, P.m_out);
+    }
     return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
 }
 // N tile: 256 activation rows when there are more than 128 (the decoded weight
@@ -434,9 +466,27 @@ extern "C" int apb_dense_prep_x(const void* x, int x_dtype, int64_t m, int64_t c
     return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
 }
 
+// Split-K factor for a launch of row_blocks x n_tiles output tiles over n_kb K
+// blocks: enough CTAs to cover the SMs (deterministic: fixed-order sum).
+static int choose_splits(int64_t tiles, int n_kb, int sms) {
+    int s = 1;
+    while (tiles * s * 2 <= (int64_t)sms && s < 8 && n_kb % (4 * s) == 0 && n_kb / (2 * s) >= 8) s *= 2;  // one wave
+    return s;
+}
+
+extern "C" int64_t apb_gemm_dense_tc_workspace(int64_t rows, int64_t padded_cols, int64_t mx) {
+    if (rows <= 0 || padded_cols <= 0 || mx <= 0) return 0;
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = ((rows + apbd::BM - 1) / apbd::BM) * ((mx + (mx > 128 ? 255 : 127)) / (mx > 128 ? 256 : 128));
+    const int sp = choose_splits(tiles, (int)(padded_cols / apbd::BK), sms);
+    return sp > 1 ? (int64_t)sp * mx * rows * 4 : 0;
+}
+
 extern "C" int apb_gemm_dense_tc(const uint8_t* planes, int n_max, int64_t rows, int64_t cols, int64_t padded_cols,
                                  int k, const uint16_t* lut, const uint16_t* xp, int64_t mx, int pairs,
-                                 const float* inv, float* y, int64_t ldy, void* stream) {
+                                 const float* inv, float* y, int64_t ldy, float* ws, int64_t ws_bytes,
+                                 void* stream) {
     using namespace apbd;
     if (!planes || !lut || !xp || !y || (pairs && !inv)) return APB_ERR_PARAM;
     if (k < 2 || k > n_max || n_max > 8) return APB_ERR_PARAM;
@@ -473,8 +523,18 @@ extern "C" int apb_gemm_dense_tc(const uint8_t* planes, int n_max, int64_t rows,
     P.ldy = ldy;
     P.mx = (int)mx;
     P.m_out = (int)m_out;
-    P.n_kb = (int)(padded_cols / BK);
     P.pairs = pairs ? 1 : 0;
+    {
+        int sms = 148, dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int bn = mx > 128 ? 256 : 128;
+        const int64_t tiles = ((rows + BM - 1) / BM) * ((mx + bn - 1) / bn);
+        int sp = choose_splits(tiles, (int)(padded_cols / BK), sms);
+        if (sp > 1 && (!ws || ws_bytes < (int64_t)sp * mx * rows * 4)) sp = 1;  // no workspace: one pass
+        P.splits = sp;
+        P.ws = ws;
+        P.n_kb = (int)(padded_cols / BK) / sp;
+    }
     cudaStream_t s = (cudaStream_t)stream;
     switch (k) {
         case 2: return launch<2>(P, rows, s);

@@ -538,9 +538,11 @@ def _dense_fused(torch, prep: PreparedLayer, k: int, x, x_is_fp16: bool):
     check(L.apb_dense_prep_x(dev.ptr(xin), dt, m, t.cols, xin.shape[1], dev.ptr(xp), t.padded_cols,
                              dev.ptr(inv), s), "apb_dense_prep_x")
     y = torch.empty((m, t.rows), dtype=torch.float32, device="cuda")
+    wsb = L.apb_gemm_dense_tc_workspace(t.rows, t.padded_cols, mx)  # split-K partials (small batches)
+    ws = torch.empty(max(wsb // 4, 1), dtype=torch.float32, device="cuda")
     check(L.apb_gemm_dense_tc(dev.ptr(t.planes), t.n_max, t.rows, t.cols, t.padded_cols, k,
                               dev.ptr(prep.tables16[k]), dev.ptr(xp), mx, pairs, dev.ptr(inv), dev.ptr(y),
-                              t.rows, s), "apb_gemm_dense_tc")
+                              t.rows, dev.ptr(ws), wsb, s), "apb_gemm_dense_tc")
     return y
 
 

@@ -86,12 +86,12 @@ def test_host_validation_before_launch(lib):
     assert lib.apb_dense_prep_x(fake, F32, 4, 1000, 1000, fake, 1024, nul, nul) == 2   # fp32 needs inv
     assert lib.apb_dense_prep_x(fake, 7, 4, 1000, 1000, fake, 1024, fake, nul) == 2    # dtype
     assert lib.apb_dense_prep_x(fake, F16, 0, 1000, 1000, fake, 1024, nul, nul) == 1   # empty batch
-    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 9, fake, fake, 64, 1, fake, fake, 16, nul) == 2  # k
-    assert lib.apb_gemm_dense_tc(fake, 4, 16, 1024, 1024, 5, fake, fake, 64, 1, fake, fake, 16, nul) == 2  # k > n_max
-    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1000, 4, fake, fake, 64, 1, fake, fake, 16, nul) == 1  # padded
-    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 63, 1, fake, fake, 16, nul) == 1  # odd pairs
-    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 64, 1, nul, fake, 16, nul) == 2  # pairs need inv
-    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 64, 0, nul, fake, 8, nul) == 1   # ldy < rows
+    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 9, fake, fake, 64, 1, fake, fake, 16, nul, 0, nul) == 2  # k
+    assert lib.apb_gemm_dense_tc(fake, 4, 16, 1024, 1024, 5, fake, fake, 64, 1, fake, fake, 16, nul, 0, nul) == 2  # k > n_max
+    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1000, 4, fake, fake, 64, 1, fake, fake, 16, nul, 0, nul) == 1  # padded
+    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 63, 1, fake, fake, 16, nul, 0, nul) == 1  # odd pairs
+    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 64, 1, nul, fake, 16, nul, 0, nul) == 2  # pairs need inv
+    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 64, 0, nul, fake, 8, nul, 0, nul) == 1   # ldy < rows
 
 
 def test_status_mapping():

@@ -782,3 +782,43 @@ def test_dense_tcgen05_vs_dense_oracle(api, m, rows, cols):
         assert ora.rel_err(y, X.astype(np.float64) @ W.T) < TOL, (k, ora.rel_err(y, X.astype(np.float64) @ W.T))
         y16 = engine.gemm(prep, X, engine.GemvConfig(bit_width=k, dense_threshold=16, activations_fp16=True))
         assert ora.rel_err(y16, X16 @ W.T) < TOL, k
+
+
+def test_dense_tcgen05_split_k_deterministic(api):
+    """Small-batch dense launches split K across CTAs (apb_gemm_dense_tc_workspace
+    > 0 for a 4096-row layer at M = 24); the fixed-order partial sum keeps the
+    result bit-identical across calls and equal to the single-pass kernel (no
+    workspace) within fp32 reassociation, and within 1e-5 of the fp64 product."""
+    import torch
+
+    from paper_2402_10517_b200 import _lib
+
+    _, _, engine, _ = api
+    L = _lib.load()
+    layer = _random_layer(api, 4242, 4096, 4096, 3, 8)
+    prep = engine.prepare(layer)
+    t = prep.tensor
+    assert L.apb_gemm_dense_tc_workspace(t.rows, t.padded_cols, 48) > 0
+    X = np.random.default_rng(7).standard_normal((24, 4096)).astype(np.float32)
+    cfg = engine.GemvConfig(bit_width=5, dense_threshold=16)
+    y1 = engine.gemm(prep, X, cfg)
+    y2 = engine.gemm(prep, X, cfg)
+    assert np.array_equal(y1, y2)
+    W = engine.dequantize(layer, 5).astype(np.float64)
+    assert ora.rel_err(y1, X.astype(np.float64) @ W.T) < TOL
+    # the same call without a workspace runs single-pass
+    xd = torch.from_numpy(X).cuda()
+    xp = torch.empty((48, t.padded_cols), dtype=torch.float16, device="cuda")
+    inv = torch.empty(24, dtype=torch.float32, device="cuda")
+    from paper_2402_10517_b200 import _device as dev
+
+    _lib.check(L.apb_dense_prep_x(dev.ptr(xd), 0, 24, 4096, 4096, dev.ptr(xp), t.padded_cols, dev.ptr(inv),
+                                  dev.stream_ptr()), "prep")
+    y0 = torch.empty((24, t.rows), dtype=torch.float32, device="cuda")
+    _lib.check(L.apb_gemm_dense_tc(dev.ptr(t.planes), t.n_max, t.rows, t.cols, t.padded_cols, 5,
+                                   dev.ptr(prep.tables16[5]), dev.ptr(xp), 48, 1, dev.ptr(inv), dev.ptr(y0), t.rows,
+                                   None, 0, dev.stream_ptr()), "dense")
+    torch.cuda.synchronize()
+    # single pass vs split K: fp32 reassociation of the (scaled) hi/lo products only
+    assert ora.rel_err(y0.cpu().numpy(), X.astype(np.float64) @ W.T) < TOL
+    assert ora.rel_err(y0.cpu().numpy(), y1) < 2e-5
