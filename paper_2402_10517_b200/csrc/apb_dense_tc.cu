@@ -45,24 +45,36 @@ namespace apbd {
 using apb::prmt;
 
 constexpr int BM = 128, BK = 64;
-constexpr int kASlots = 2, kPStages = 2;
 constexpr int kDecWarps = 16;  // (row quarter q, word h, K-block parity) -- 4 per SM sub-partition
 constexpr int kThreads = (2 + kDecWarps) * 32;
 constexpr int kSmemBase = 1024;  // sm_100 reserves the first 1 KB of the shared window
-constexpr int kTableMax = 64 * 1024;
 // dynamic shared memory layout (offsets from the 1024-aligned base), per N tile
-template <int BN>
+template <int BN, int K>
 struct Lay {
     static constexpr int kXStages = BN == 256 ? 4 : 6;
+    static_assert(BN == 32 || BN == 64 || BN == 128 || BN == 256, "UMMA N tile");
     static constexpr int kOffX = 0;                              // activation tiles (BN x 128 B)
-    static constexpr int kOffP = kOffX + kXStages * BN * 128;    // plane chunks (k x 2 KB)
-    static constexpr int kOffT = kOffP + kPStages * 8 * 2048;    // centroid table (<= 64 KB)
-    static constexpr int kOffB = kOffT + kTableMax;              // mbarriers + TMEM address
-    static constexpr int kBytes = kOffB + 256;
+    // centroid table: u32 [2^k][128 rows] (k <= 7), u16 (k = 8)
+    static constexpr int kTableBytes = (1 << K) * (K <= 7 ? 4 : 2) * BM;
+    // plane chunk ring: as many K x 2 KB stages as the budget leaves (2..8): each
+    // stage covers two K blocks, and DRAM latency must hide behind the others
+    static constexpr int kPStride = K * 2048;
+    static constexpr int kPBudget = 227 * 1024 - 512 - kXStages * BN * 128 - kTableBytes;
+    static constexpr int kPStages = kPBudget / kPStride > 8 ? 8 : kPBudget / kPStride;
+    static_assert(kPStages >= 2, "plane ring");
+    static constexpr int kOffP = kOffX + kXStages * BN * 128;    // plane chunks
+    static constexpr int kOffT = kOffP + kPStages * kPStride;    // centroid table
+    static constexpr int kOffB = (kOffT + kTableBytes + 15) / 16 * 16;  // mbarriers + TMEM address
+    static constexpr int kBytes = kOffB + 512;
     static constexpr uint32_t kTable = (uint32_t)(kSmemBase + kOffT);  // absolute (LDS immediate)
     // tensor memory: D = columns [0, BN) (fp32), decoded A slots of 32 columns each
     // (128 lanes = weight rows x 64 K as packed fp16 pairs) after it
-    static constexpr int kTmemCols = BN == 256 ? 512 : 256;
+    static constexpr int kTmemCols = BN == 256 ? 512 : 256;  // power of two >= columns used
+    // decoded A slots (32 TMEM columns each): 4 with the 128-wide N tile (small
+    // batches are decode-bound: four K blocks in flight, each decoder warp owns
+    // every 4th K block), 2 with the 256-wide tile (TMEM: 256 + 2 x 32 <= 512)
+    static constexpr int kASlots = BN <= 128 ? 4 : 2;
+    static_assert(BN + 32 * kASlots <= kTmemCols, "tensor memory budget");
     static constexpr uint32_t kColA = BN;
 };
 
@@ -152,8 +164,8 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 
 template <int K, int BN>
 __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_constant__ DenseParams P) {
-    using Y = Lay<BN>;
-    constexpr int kXStages = Y::kXStages;
+    using Y = Lay<BN, K>;
+    constexpr int kXStages = Y::kXStages, kASlots = Y::kASlots, kPStages = Y::kPStages;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (saddr(smem) != kSmemBase) __trap();  // the table base is an LDS immediate
@@ -161,12 +173,12 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
     const int n0 = blockIdx.y * BN;
     const uint32_t sX = saddr(smem + Y::kOffX), sP = saddr(smem + Y::kOffP);
     const uint32_t bar = saddr(smem + Y::kOffB);
-    // barriers (8 B each): x_full[8] x_empty[8] a_full[2] a_empty[2] p_full[2] p_empty[2] d_full
-    static_assert(kXStages <= 8, "barrier layout");
-    const uint32_t b_xf = bar, b_xe = bar + 64, b_af = bar + 128, b_ae = bar + 144, b_pf = bar + 160,
-                   b_pe = bar + 176, b_d = bar + 192;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Y::kOffB + 240);
-    constexpr int kPlaneBytes = K * 2048;  // one plane chunk stage: 16 B x 128 rows x K planes
+    // barriers (8 B each): x_full[8] x_empty[8] a_full[4] a_empty[4] p_full[8] p_empty[8] d_full
+    static_assert(kXStages <= 8 && kASlots <= 4 && kPStages <= 8, "barrier layout");
+    const uint32_t b_xf = bar, b_xe = bar + 64, b_af = bar + 128, b_ae = bar + 160, b_pf = bar + 192,
+                   b_pe = bar + 256, b_d = bar + 320;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Y::kOffB + 336);
+    constexpr int kPlaneBytes = Y::kPStride;  // one plane chunk stage: 16 B x 128 rows x K planes
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kXStages; ++i) {
@@ -174,12 +186,12 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
             mbar_init(b_xe + 8 * i, 1);
         }
         for (int i = 0; i < kASlots; ++i) {
-            mbar_init(b_af + 8 * i, 8 * 32);  // the 8 decode warps of this K-block parity
+            mbar_init(b_af + 8 * i, (kASlots == 4 ? 4 : 8) * 32);  // the decoder warps of this K block
             mbar_init(b_ae + 8 * i, 1);
         }
         for (int i = 0; i < kPStages; ++i) {
             mbar_init(b_pf + 8 * i, 1);
-            mbar_init(b_pe + 8 * i, kDecWarps * 32);
+            mbar_init(b_pe + 8 * i, (kASlots == 4 ? 8 : kDecWarps) * 32);  // decoders of its two K blocks
         }
         mbar_init(b_d, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -197,15 +209,18 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
     const int kb0 = (int)blockIdx.z * n_kb;  // first global K block (even)
 
     if (warp == 0) {
-        // ================================ TMA producer ================================
+        // ================================ TMA producers ================================
+        // lane 0 streams plane chunks, lane 1 activation tiles: independent rings, so a
+        // full activation ring (waiting on the MMA) never stalls the plane prefetch
         if (lane == 0) {
+            for (int ps = 0; ps < (n_kb >> 1); ++ps) {  // plane chunk ps = K blocks 2ps, 2ps+1
+                const int s = ps % kPStages;
+                if (ps >= kPStages) mbar_wait(b_pe + 8 * s, ((ps / kPStages) - 1) & 1);
+                mbar_expect_tx(b_pf + 8 * s, kPlaneBytes);
+                tma3(sP + s * Y::kPStride, &P.tm_planes, 16 * ((kb0 >> 1) + ps), (int)row0, 0, b_pf + 8 * s);
+            }
+        } else if (lane == 1) {
             for (int kb = 0; kb < n_kb; ++kb) {
-                if ((kb & 1) == 0) {  // plane chunk = K blocks kb, kb+1
-                    const int ps = kb >> 1, s = ps % kPStages;
-                    if (ps >= kPStages) mbar_wait(b_pe + 8 * s, ((ps / kPStages) - 1) & 1);
-                    mbar_expect_tx(b_pf + 8 * s, kPlaneBytes);
-                    tma3(sP + s * 8 * 2048, &P.tm_planes, 16 * ((kb0 >> 1) + ps), (int)row0, 0, b_pf + 8 * s);
-                }
                 const int s = kb % kXStages;
                 if (kb >= kXStages) mbar_wait(b_xe + 8 * s, ((kb / kXStages) - 1) & 1);
                 mbar_expect_tx(b_xf + 8 * s, BN * 128);
@@ -233,8 +248,11 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
     } else {
         // =================== decoders, then the epilogue ===================
         // decode warp dw: rows 32q..32q+31 (q = warp & 3, the TMEM lane quarter this
-        // warp may read), lane word h of every K block with parity par
-        const int dw = warp - 2, q4 = warp & 3, h = (dw >> 2) & 1, par = dw >> 3;
+        // warp may write / read).  2 A slots: lane word h of every K block with parity
+        // par; 4 A slots: both lane words of every K block kb = ph (mod 4)
+        const int dw = warp - 2, q4 = warp & 3;
+        const int h = kASlots == 4 ? 0 : (dw >> 2) & 1, par = kASlots == 4 ? dw >> 2 : dw >> 3;
+        constexpr int kWords = kASlots == 4 ? 2 : 1;
         const int r = 32 * q4 + lane;
         const int64_t grow = row0 + r;
         // this row's centroid table: u32 [entry][128 rows] (k <= 7), u16 (k = 8); the
@@ -255,48 +273,52 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
         const uint32_t rr = (uint32_t)r << 1;  // byte 0 of the table address
         // this warp's TMEM lane quarter; A slot columns of word h
         const uint32_t t_row = tmem + ((uint32_t)(32 * q4) << 16) + Y::kColA + 16u * (uint32_t)h;
-        for (int kb = par; kb < n_kb; kb += 2) {
-            // this row's lane word of K block kb: plane chunk stage kb / 2, word 2 (kb & 1) + h
+        for (int kb = par; kb < n_kb; kb += (kASlots == 4 ? 4 : 2)) {
+            // this row's lane word(s) of K block kb: plane chunk stage kb / 2, words 2 (kb & 1) + h (+1)
             const int ps = kb >> 1, s = ps % kPStages;
             mbar_wait(b_pf + 8 * s, (ps / kPStages) & 1);
-            uint32_t Q[K];
+            uint32_t Q[kWords][K];
 #pragma unroll
-            for (int i = 0; i < K; ++i) {  // Q[i] = plane K-1-i (LSB plane first)
-                uint32_t v;
-                asm volatile("ld.shared.u32 %0, [%1];"
-                             : "=r"(v)
-                             : "r"(sP + s * 8 * 2048 + (K - 1 - i) * 2048 + r * 16 + (2 * (kb & 1) + h) * 4));
-                Q[i] = v;
+            for (int i = 0; i < K; ++i) {  // Q[.][i] = plane K-1-i (LSB plane first)
+                const uint32_t a = sP + s * Y::kPStride + (K - 1 - i) * 2048 + r * 16 + (2 * (kb & 1) + h) * 4;
+                if constexpr (kWords == 2) {
+                    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(Q[0][i]), "=r"(Q[kWords - 1][i]) : "r"(a));
+                } else {
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(Q[0][i]) : "r"(a));
+                }
             }
             mbar_arrive(b_pe + 8 * s);
-            uint32_t W[8];
-            apb::to_bytes<K>(Q, W);  // W[b] byte p = code of column 256p + 8t + b
-            uint32_t v[16];          // K elements 32h + 8p + b as fp16 pairs: column 4p + b/2 of word h
-#pragma unroll
-            for (int p = 0; p < 4; ++p)
-#pragma unroll
-                for (int b = 0; b < 8; b += 2) {
-                    const uint32_t a0 = prmt(W[b], rr, 0x7604u | (uint32_t)(p << 4));  // code << 8 | r << 1
-                    const uint32_t a1 = prmt(W[b + 1], rr, 0x7604u | (uint32_t)(p << 4));
-                    uint32_t lo, hi;
-                    if constexpr (K <= 7) {
-                        lo = lds_t32<Y::kTable>(a0 << 1);
-                        hi = lds_t32<Y::kTable>(a1 << 1);
-                    } else {
-                        lo = lds_t16<Y::kTable>(a0);
-                        hi = lds_t16<Y::kTable>(a1);
-                    }
-                    v[4 * p + b / 2] = lo | (hi << 16);
-                }
-            const int sa = kb % kASlots;  // == par
+            const int sa = kb % kASlots;
             if (kb >= kASlots) mbar_wait(b_ae + 8 * sa, ((kb / kASlots) - 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            asm volatile(
-                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-                    t_row + 32u * (uint32_t)sa),
-                "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
-                "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-                : "memory");
+#pragma unroll
+            for (int w = 0; w < kWords; ++w) {
+                uint32_t W[8];
+                apb::to_bytes<K>(Q[w], W);  // W[b] byte p = code of column 256p + 8t + b
+                uint32_t v[16];             // K elements 32h + 8p + b as fp16 pairs: column 4p + b/2 of word h
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int b = 0; b < 8; b += 2) {
+                        const uint32_t a0 = prmt(W[b], rr, 0x7604u | (uint32_t)(p << 4));  // code << 8 | r << 1
+                        const uint32_t a1 = prmt(W[b + 1], rr, 0x7604u | (uint32_t)(p << 4));
+                        uint32_t lo, hi;
+                        if constexpr (K <= 7) {
+                            lo = lds_t32<Y::kTable>(a0 << 1);
+                            hi = lds_t32<Y::kTable>(a1 << 1);
+                        } else {
+                            lo = lds_t16<Y::kTable>(a0);
+                            hi = lds_t16<Y::kTable>(a1);
+                        }
+                        v[4 * p + b / 2] = lo | (hi << 16);
+                    }
+                asm volatile(
+                    "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+                        t_row + 32u * (uint32_t)sa + 16u * (uint32_t)w),
+                    "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+                    "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+                    : "memory");
+            }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(b_af + 8 * sa);
@@ -305,30 +327,46 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
         // the 4 warp groups (dw >> 2) split the BN accumulator columns
         mbar_wait(b_d, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        constexpr int kCols = BN / 4;
+        constexpr int kCols = BN / 4;                  // accumulator columns per warp group
+        constexpr int kChunk = kCols < 32 ? kCols : 32;  // tcgen05.ld .x8 / .x16 / .x32
 #pragma unroll 1
-        for (int c0 = (dw >> 2) * kCols; c0 < ((dw >> 2) + 1) * kCols; c0 += 32) {
+        for (int c0 = (dw >> 2) * kCols; c0 < ((dw >> 2) + 1) * kCols; c0 += kChunk) {
             uint32_t d[32];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
-                  "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]),
-                  "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]),
-                  "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]),
-                  "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
-                : "r"(tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)c0));
+            const uint32_t ta = tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)c0;
+            if constexpr (kChunk == 32) {
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+                      "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]),
+                      "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]),
+                      "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]),
+                      "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
+                    : "r"(ta));
+            } else if constexpr (kChunk == 16) {
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                    : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+                      "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]),
+                      "=r"(d[15])
+                    : "r"(ta));
+            } else {
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                             : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]),
+                               "=r"(d[7])
+                             : "r"(ta));
+            }
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (grow < P.rows && P.splits > 1) {  // split-K: raw partial tile, summed by split_sum_kernel
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
+                for (int c = 0; c < kChunk; ++c) {
                     const int n = n0 + c0 + c;
                     if (n < P.mx) P.ws[((int64_t)blockIdx.z * P.mx + n) * P.rows + grow] = __uint_as_float(d[c]);
                 }
             } else if (grow < P.rows) {
                 if (P.pairs) {  // columns (2i, 2i+1) = (hi, lo) of output row (n0 + c) / 2
 #pragma unroll
-                    for (int c = 0; c < 32; c += 2) {
+                    for (int c = 0; c < kChunk; c += 2) {
                         const int m = (n0 + c0 + c) >> 1;
                         if (m < P.m_out)
                             P.y[(int64_t)m * P.ldy + grow] =
@@ -336,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
                     }
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
+                    for (int c = 0; c < kChunk; ++c) {
                         const int m = n0 + c0 + c;
                         if (m < P.m_out) P.y[(int64_t)m * P.ldy + grow] = __uint_as_float(d[c]);
                     }
@@ -430,10 +468,10 @@ static EncodeTiledFn encode_fn() {
 template <int K, int BN>
 static int launch_bn(DenseParams& P, int64_t rows, cudaStream_t s) {
     static std::atomic<unsigned long long> configured{0};
-    static_assert(Lay<BN>::kBytes <= 227 * 1024, "shared memory budget");
-    if (!apb::ensure_smem_optin(dense_tc_kernel<K, BN>, Lay<BN>::kBytes, configured)) return APB_ERR_CUDA;
+    static_assert(Lay<BN, K>::kBytes <= 227 * 1024, "shared memory budget");
+    if (!apb::ensure_smem_optin(dense_tc_kernel<K, BN>, Lay<BN, K>::kBytes, configured)) return APB_ERR_CUDA;
     const dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((P.mx + BN - 1) / BN), (unsigned)P.splits);
-    dense_tc_kernel<K, BN><<<grid, kThreads, Lay<BN>::kBytes, s>>>(P);
+    dense_tc_kernel<K, BN><<<grid, kThreads, Lay<BN, K>::kBytes, s>>>(P);
     if (cudaGetLastError() != cudaSuccess) return APB_ERR_CUDA;
     if (P.splits > 1) {
         const int64_t n = (int64_t)P.m_out * rows;
@@ -442,11 +480,18 @@ static int launch_bn(DenseParams& P, int64_t rows, cudaStream_t s) {
     }
     return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
 }
-// N tile: 256 activation rows when there are more than 128 (the decoded weight
-// tile then feeds twice the MMA work), else 128
+// N tile: the activation rows rounded up to 32 / 64 / 128, or 256 above 128 (a
+// decoded weight tile then feeds twice the MMA work); small batches stage only
+// the rows they have (the activation tile is shared-memory traffic per K block)
+static int pick_bn(int64_t mx) { return mx > 128 ? 256 : (mx > 64 ? 128 : (mx > 32 ? 64 : 32)); }
 template <int K>
 static int launch(DenseParams& P, int64_t rows, cudaStream_t s) {
-    return P.mx > 128 ? launch_bn<K, 256>(P, rows, s) : launch_bn<K, 128>(P, rows, s);
+    switch (pick_bn(P.mx)) {
+        case 32: return launch_bn<K, 32>(P, rows, s);
+        case 64: return launch_bn<K, 64>(P, rows, s);
+        case 128: return launch_bn<K, 128>(P, rows, s);
+    }
+    return launch_bn<K, 256>(P, rows, s);
 }
 
 }  // namespace apbd
@@ -478,7 +523,8 @@ extern "C" int64_t apb_gemm_dense_tc_workspace(int64_t rows, int64_t padded_cols
     if (rows <= 0 || padded_cols <= 0 || mx <= 0) return 0;
     int sms = 148, dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t tiles = ((rows + apbd::BM - 1) / apbd::BM) * ((mx + (mx > 128 ? 255 : 127)) / (mx > 128 ? 256 : 128));
+    const int bn = apbd::pick_bn(mx);
+    const int64_t tiles = ((rows + apbd::BM - 1) / apbd::BM) * ((mx + bn - 1) / bn);
     const int sp = choose_splits(tiles, (int)(padded_cols / apbd::BK), sms);
     return sp > 1 ? (int64_t)sp * mx * rows * 4 : 0;
 }
@@ -500,7 +546,7 @@ extern "C" int apb_gemm_dense_tc(const uint8_t* planes, int n_max, int64_t rows,
     {
         const cuuint64_t dims[2] = {(cuuint64_t)padded_cols, (cuuint64_t)mx};
         const cuuint64_t strides[1] = {(cuuint64_t)padded_cols * 2};
-        const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)(mx > 128 ? 256 : 128)}, es[2] = {1, 1};  // N tile (launch)
+        const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)pick_bn(mx)}, es[2] = {1, 1};  // N tile (launch)
         if (enc(&P.tm_x, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)xp, dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -527,7 +573,7 @@ extern "C" int apb_gemm_dense_tc(const uint8_t* planes, int n_max, int64_t rows,
     {
         int sms = 148, dev = 0;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int bn = mx > 128 ? 256 : 128;
+        const int bn = pick_bn(mx);
         const int64_t tiles = ((rows + BM - 1) / BM) * ((mx + bn - 1) / bn);
         int sp = choose_splits(tiles, (int)(padded_cols / BK), sms);
         if (sp > 1 && (!ws || ws_bytes < (int64_t)sp * mx * rows * 4)) sp = 1;  // no workspace: one pass
