@@ -90,7 +90,11 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ c
         orv |= (orv >> 8);
         orv &= 0xFFu;
         orv = __reduce_or_sync(0xFFFFFFFFu, orv);
-        if ((threadIdx.x & 31) == 0 && orv) atomicOr(code_or, orv);
+        // only bits not yet recorded go to the (single, shared) word: after the
+        // first few warps every code bit is usually set and no atomic is issued
+        // (one atomicOr per warp serialised ~230K atomics on one address for a
+        // 28672x8192 matrix)
+        if ((threadIdx.x & 31) == 0 && (orv & ~__ldcg(code_or))) atomicOr(code_or, orv);
     }
 }
 

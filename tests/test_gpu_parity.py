@@ -105,6 +105,14 @@ def test_pack_errors(api):
         bitplane.pack_bitplanes(np.array([[8]]), 3)
     with pytest.raises(errors.CodeRangeError):  # only the device OR-flag can see this one
         bitplane.pack_bitplanes(np.array([[1, 2, 200]], dtype=np.uint8), 7)
+    # a single out-of-range code deep in a large matrix: the kernel skips the
+    # shared atomic once a bit is recorded, so a NEW bit must still get through
+    big = np.random.default_rng(3).integers(0, 1 << 7, size=(3000, 5000), dtype=np.uint8)
+    big[2999, 4999] = 200
+    with pytest.raises(errors.CodeRangeError):
+        bitplane.pack_permuted(big, 7)
+    big[2999, 4999] = 100
+    bitplane.pack_permuted(big, 7)  # in range: no error
     with pytest.raises(errors.ShapeError):
         bitplane.pack_bitplanes(np.zeros((0, 4), dtype=np.uint8), 3)
     with pytest.raises(errors.ParameterError):
