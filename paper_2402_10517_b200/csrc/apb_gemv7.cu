@@ -882,6 +882,9 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
 #pragma unroll
         for (int i = 0; i < 8; ++i) xv[b][i] = 0u;
 
+#ifdef APB_TIMELINE
+    long long full_wait = 0, t_begin = clock64();
+#endif
     int pi = problem_of(L, first), pend = problem_end(L, pi), xb = 0;
     uint32_t xph = 0;  // bit b: phase parity of x buffer b
     int gs = grp;            // next ring stage of this warp group
@@ -955,7 +958,15 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
 #pragma unroll 1
         for (; gs < item_gs + nt; gs += NG) {
             const int tile = gs - item_gs;
+#ifdef APB_TIMELINE
+            {
+                const long long w0 = clock64();
+                mbar_sleep(b_full + 8 * slot, ph);
+                full_wait += clock64() - w0;
+            }
+#else
             mbar_sleep(b_full + 8 * slot, ph);
+#endif
             if (warp == 0 && lane == 0 && gs == 0) APB_TL(3);
             const uint32_t sb = s_ring + slot * G::kStageBytes;
             // one tile of this warp's chunks; TAIL: the last, partial tile of a layer
@@ -1044,6 +1055,12 @@ __global__ void __launch_bounds__(Geo<K, NB, CPS>::kThreads, CPS) gemv7_kernel(c
         mbar_arrive(b_idone + 8 * (jl & 1));  // all lanes (release orders the partial stores)
         if (warp == 0 && lane == 0 && jl == 0) APB_TL(4);
     }
+#ifdef APB_TIMELINE
+    if (warp == 0 && lane == 0) {  // slot 7: warp 0's cycles waiting for plane stages / cycles in its loop
+        g_tl7[((size_t)(L.tl_launch % 64) * 512 + blockIdx.x) * 8 + 7] =
+            ((unsigned long long)full_wait << 32) | (unsigned long long)((clock64() - t_begin) & 0xFFFFFFFFull);
+    }
+#endif
 }
 
 // ---- host side -------------------------------------------------------------------

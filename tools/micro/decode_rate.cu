@@ -141,11 +141,12 @@ __device__ __forceinline__ void mbar_init2(uint32_t a, uint32_t n) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
 }
 __device__ __forceinline__ void mbar_wait2(uint32_t a, uint32_t parity) {
-    asm volatile("{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
+    // try_wait with a suspend-time hint: the waiting thread sleeps in the barrier unit
+    asm volatile("{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t@!p bra W_%=;\n\t}" ::"r"(a), "r"(parity), "r"(1000000) : "memory");
 }
 __device__ CUtensorMap g_tmap_c;
 __device__ const CUtensorMap* g_tmap;
-template <int K, int MODE>
+template <int K, int MODE, int SZ = 4096>
 __global__ void __launch_bounds__(640, 1) map0s(int iters, float* out, const uint4* src, size_t n16) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ int done_cnt;
@@ -157,6 +158,12 @@ __global__ void __launch_bounds__(640, 1) map0s(int iters, float* out, const uin
     if (warp >= 16) {
         if (MODE == 2 && warp > 16) return;
         if (MODE == 0) return;
+        if (MODE == 6) {  // control: one thread polling the stop flag with nanosleep, no copies
+            if (warp != 16 || lane != 0) return;
+            while (*stop < 16) __nanosleep(2000);
+            out[(1 << 21) + blockIdx.x * 2] = 0.f;
+            return;
+        }
         uint32_t accx = 0;
         size_t i = ((size_t)blockIdx.x * 2 + (warp - 16)) * 32 * 8 + lane;
         const size_t stride = (size_t)gridDim.x * 2 * 32 * 8;
@@ -184,7 +191,7 @@ __global__ void __launch_bounds__(640, 1) map0s(int iters, float* out, const uin
         } else {
             if (warp != 16 || lane != 0) return;
             // 16 x 4 KB ring at [kXOff - 64 KB, kXOff), barriers after the planes region
-            constexpr int NR = 16;
+            constexpr int NR = 65536 / SZ > 16 ? 16 : 65536 / SZ;
             const uint32_t ring = saddr(smem + kXOff - 65536), bar = saddr(smem + kPlaneOff - 256);
             for (int j = 0; j < NR; ++j) mbar_init2(bar + 8 * j, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -195,10 +202,10 @@ __global__ void __launch_bounds__(640, 1) map0s(int iters, float* out, const uin
             while (*stop < 16) {
                 const int j = it % NR;
                 if (it >= NR) mbar_wait2(bar + 8 * j, ((it / NR) - 1) & 1);
-                asm volatile("{\n\t.reg .b64 s;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 s, [%0], %1;\n\t}" ::"r"(bar + 8 * j), "r"(4096) : "memory");
+                asm volatile("{\n\t.reg .b64 s;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 s, [%0], %1;\n\t}" ::"r"(bar + 8 * j), "r"(MODE == 2 ? SZ : 4096) : "memory");
                 if (MODE == 2) {
-                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(ring + 4096 * j),
-                                 "l"((const char*)src + off % (n16 * 16 - 4096)), "r"(4096), "r"(bar + 8 * j) : "memory");
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(ring + SZ * j),
+                                 "l"((const char*)src + off % (n16 * 16 - SZ)), "r"(SZ), "r"(bar + 8 * j) : "memory");
                 } else {
                     // two 2 KB boxes {128 B, 16 rows, 1 plane} of a [8 planes][rows][1024 B] u8 tensor, 128B swizzle
                     for (int h = 0; h < 2; ++h)
@@ -206,8 +213,8 @@ __global__ void __launch_bounds__(640, 1) map0s(int iters, float* out, const uin
                                      "l"(g_tmap), "r"((int)((it * 2 + h) % 8) * 128), "r"(row % 65536), "r"(h), "r"(bar + 8 * j) : "memory");
                     row += 16 * 148;
                 }
-                off += (size_t)gridDim.x * 4096;
-                bytes += 4096;
+                off += (size_t)gridDim.x * (MODE == 2 ? SZ : 4096);
+                bytes += MODE == 2 ? SZ : 4096;
                 ++it;
             }
             for (int j = 0; j < NR && j < it; ++j) mbar_wait2(bar + 8 * ((it - 1 - j) % NR), ((it - 1 - j) / NR) & 1);
@@ -372,10 +379,10 @@ static void suite() {
     run("map1 lane=row", map1<K, PACK>, K, 2048, 16, 1);
 }
 
-template <int K, int MODE>
+template <int K, int MODE, int SZ = 4096>
 static int run_stream(const char* name) {
     const int smem = 227 * 1024 - 2048;
-    auto kern = map0s<K, MODE>;
+    auto kern = map0s<K, MODE, SZ>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     float* out;
     CK(cudaMalloc(&out, (4 << 20) * 4));
@@ -415,27 +422,99 @@ static int run_stream(const char* name) {
     return 0;
 }
 
+
+// MAP 0 with a compact shared-memory layout (table | x | planes) so that CPS CTAs
+// of W warps fit per SM: tests the shipped configuration (2 CTAs x 8 warps, <= 96 regs)
+template <int K, int W, int CPS>
+__global__ void __launch_bounds__(W * 32, CPS) map0c(int iters, float* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr int kTab = (K <= 4 ? (1 << (2 * K)) : (1 << K)) * 256;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, q = lane & 3, rho = 2 * g + (q >> 1), cp = q & 1, su = warp & 3;
+    const int NST = 4;
+    uint32_t plane_off[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) plane_off[j] = rho * 128 + (((su + 4 * j) ^ (rho & 7)) << 4) + cp * 8;
+    const int gset = (g >> 1) & 1;
+    const uint32_t xlive = (q >> 1) == (g & 1) && (g >> 2) == 0;
+    const uint32_t xrow = saddr(smem + kTab) + (uint32_t)(32 * su + 16 * cp + 4 * gset) * 2u;
+    const uint32_t off = (uint32_t)lane * 4u;
+    uint32_t xv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    float acc[2][4] = {};
+    const uint32_t ring = saddr(smem + kTab + 8192);
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int it = 0; it < iters; ++it) {
+        const uint32_t sb = ring + (uint32_t)((it + (warp >> 2)) % NST) * (K * 2048);
+        const int tile = it & 3;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            uint2 pv[K];
+#pragma unroll
+            for (int p = 0; p < K; ++p) pv[K - 1 - p] = lds64(sb + p * 2048 + plane_off[j]);
+#pragma unroll
+            for (int wi = 0; wi < 2; ++wi) {
+                const uint32_t xa = xrow + (uint32_t)(tile * 1024 + 128 * j + 8 * wi) * 2u;
+#pragma unroll
+                for (int p = 0; p < 4; ++p) lds64_keep(xv[2 * p], xv[2 * p + 1], xa + 512 * p, xlive);
+                uint32_t Q[K];
+#pragma unroll
+                for (int i = 0; i < K; ++i) Q[i] = wi ? pv[i].y : pv[i].x;
+                uint32_t a[16], a2[16];
+                decode<K, 1>(Q, off, a, a2);
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+                    mma16816(acc[p & 1], a[p * 4 + 0], a[p * 4 + 2], a[p * 4 + 1], a[p * 4 + 3], xv[2 * p], xv[2 * p + 1]);
+            }
+        }
+    }
+    long long t1 = clock64();
+    float sacc = 0;
+    for (int i = 0; i < 4; ++i) sacc += acc[0][i] + acc[1][i];
+    out[blockIdx.x * blockDim.x + tid] = sacc;
+    if (tid == 0) out[1 << 20 | blockIdx.x] = (float)(t1 - t0);
+}
+
+template <int K, int W, int CPS>
+static int run_c(const char* name) {
+    constexpr int kTab = (K <= 4 ? (1 << (2 * K)) : (1 << K)) * 256;
+    const int smem = kTab + 8192 + 4 * K * 2048 + 1024;
+    auto kern = map0c<K, W, CPS>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    float* out;
+    CK(cudaMalloc(&out, (2 << 20) * 4));
+    const int iters = 4000;
+    kern<<<148 * CPS, W * 32, smem>>>(16, out);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    kern<<<148 * CPS, W * 32, smem>>>(iters, out);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    int clk;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    const double w = (double)148 * CPS * W * iters * 4096;
+    const double wpc = w / 148 / (ms * 1e-3 * clk * 1e3);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, kern);
+    printf("%-28s k=%d %d CTA x %2d warps (%d regs, %d B smem): %6.1f w/clk/SM\n", name, K, CPS, W, fa.numRegs, smem, wpc);
+    cudaFree(out);
+    return 0;
+}
+
 int main() {
     uint32_t* dummy;
     cudaMalloc(&dummy, 4);
-    run_stream<5, 0>("map0 no stream");
-    run_stream<5, 2>("map0 + TMA bulk stream");
-    run_stream<5, 4>("map0 + TMA tensor 3D swz");
-    run_stream<3, 0>("map0 no stream");
-    run_stream<3, 4>("map0 + TMA tensor 3D swz");
-    run_stream<8, 0>("map0 no stream");
-    run_stream<8, 2>("map0 + TMA bulk stream");
-    run_stream<8, 4>("map0 + TMA tensor 3D swz");
-    run_stream<3, 2>("map0 + TMA bulk stream");
-    return 0;
-    suite<3, 1>();
-    suite<4, 1>();
-    suite<5, 1>();
-    run("map0 nopack", map0<5, 0>, 5, 4096, 16, 1);
-    run("map1 nopack", map1<5, 0>, 5, 2048, 16, 1);
-    suite<6, 1>();
-    suite<8, 1>();
-    run("map0 nopack", map0<8, 0>, 8, 4096, 16, 1);
-    run("map1 nopack", map1<8, 0>, 8, 2048, 16, 1);
+    run_c<3, 16, 1>("compact 1x16");
+    run_c<3, 8, 2>("compact 2x8 (shipped shape)");
+    run_c<3, 16, 2>("compact 2x16");
+    run_c<5, 16, 1>("compact 1x16");
+    run_c<5, 8, 2>("compact 2x8");
+    run_c<8, 16, 1>("compact 1x16");
+    run_c<8, 12, 1>("compact 1x12 (shipped k=8)");
     return 0;
 }
