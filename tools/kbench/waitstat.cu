@@ -23,15 +23,18 @@ int main() {
             cudaDeviceSynchronize();
             std::vector<unsigned long long> t(64 * 512 * 8);
             apb7_read_timeline(t.data(), 64 * 512 * 8);
-            double fr = 0; int n = 0; double mx = 0;
+            double fr = 0; int n = 0; double mx = 0, cyc = 0;
             for (int c = 0; c < 512; ++c) {
                 unsigned long long v = t[(size_t)c * 8 + 7];
                 if (!v) continue;
                 double wait = (double)(v >> 32), tot = (double)(v & 0xFFFFFFFFull);
-                if (tot > 0) { fr += wait / tot; ++n; mx = std::max(mx, wait / tot); }
+                if (tot > 0) { fr += wait / tot; ++n; mx = std::max(mx, wait / tot); cyc += tot; }
             }
-            printf("%lldx%lld k=%d: warp-0 time waiting for plane stages: mean %.1f %% (max %.1f %%) over %d CTAs\n",
-                   (long long)R, (long long)C, k, n ? 100 * fr / n : 0.0, 100 * mx, n);
+            // in-loop rate: a CTA's weights over its loop cycles, x CTAs per SM (n / 148)
+            const double wpc = n ? ((double)R * C / n) / (cyc / n) * ((double)n / 148) : 0;
+            printf("%lldx%lld k=%d: warp-0 time waiting for plane stages: mean %.1f %% (max %.1f %%) over %d CTAs; "
+                   "in-loop rate %.1f w/clk/SM (loop %.1f us avg)\n",
+                   (long long)R, (long long)C, k, n ? 100 * fr / n : 0.0, 100 * mx, n, wpc, n ? cyc / n / 1965.0 : 0.0);
         }
         cudaFree(planes); cudaFree(lut); cudaFree(x); cudaFree(y);
     }
