@@ -830,3 +830,17 @@ def test_dense_tcgen05_split_k_deterministic(api):
     # single pass vs split K: fp32 reassociation of the (scaled) hi/lo products only
     assert ora.rel_err(y0.cpu().numpy(), X.astype(np.float64) @ W.T) < TOL
     assert ora.rel_err(y0.cpu().numpy(), y1) < 2e-5
+
+
+def test_dense_tcgen05_small_parent_and_rows(api):
+    """Dense tcgen05 path with an n_max = 5 parent (the plane-chunk TMA map has 5
+    planes) and a 33-row layer (one partial 128-row tile), k = 2..5, against the
+    fp64 product of the reference dequantisation."""
+    _, _, engine, _ = api
+    layer = _random_layer(api, 4343, 33, 1500, 2, 5)
+    prep = engine.prepare(layer)
+    X = np.random.default_rng(11).standard_normal((40, 1500)).astype(np.float32)
+    for k in range(2, 6):
+        W = engine.dequantize(layer, k).astype(np.float64)
+        y = engine.gemm(prep, X, engine.GemvConfig(bit_width=k, dense_threshold=16))
+        assert ora.rel_err(y, X.astype(np.float64) @ W.T) < TOL, k
