@@ -540,6 +540,9 @@ extern "C" int apb_gemm_dense_tc(const uint8_t* planes, int n_max, int64_t rows,
         return APB_ERR_SHAPE;
     const int64_t m_out = pairs ? mx / 2 : mx;
     if (ldy < rows || mx > INT32_MAX) return APB_ERR_SHAPE;
+    if (((uintptr_t)planes & 15) || ((uintptr_t)xp & 15)) return APB_ERR_PARAM;  // TMA global addresses
+    if ((mx + pick_bn(mx) - 1) / pick_bn(mx) > 65535) return APB_ERR_SHAPE;       // grid.y
+    if (ws && ((uintptr_t)ws & 3)) return APB_ERR_PARAM;
     EncodeTiledFn enc = encode_fn();
     if (!enc) return APB_ERR_CUDA;
     DenseParams P = {};

@@ -92,6 +92,9 @@ def test_host_validation_before_launch(lib):
     assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 63, 1, fake, fake, 16, nul, 0, nul) == 1  # odd pairs
     assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 64, 1, nul, fake, 16, nul, 0, nul) == 2  # pairs need inv
     assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, fake, 64, 0, nul, fake, 8, nul, 0, nul) == 1   # ldy < rows
+    odd = ctypes.c_void_p(0x1008)  # not 16-byte aligned: a TMA operand
+    assert lib.apb_gemm_dense_tc(odd, 8, 16, 1024, 1024, 4, fake, fake, 64, 0, nul, fake, 16, nul, 0, nul) == 2
+    assert lib.apb_gemm_dense_tc(fake, 8, 16, 1024, 1024, 4, fake, odd, 64, 0, nul, fake, 16, nul, 0, nul) == 2
 
 
 def test_status_mapping():
