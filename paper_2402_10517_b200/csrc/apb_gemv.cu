@@ -1008,18 +1008,10 @@ static int launch6(const GemvLaunch& L, cudaStream_t s) {
     return cudaGetLastError() == cudaSuccess ? APB_OK : APB_ERR_CUDA;
 }
 
-static bool use_v6() {
-    static const int v = [] {
-        const char* e = std::getenv("APB_GEMV_V5");
-        return (e && e[0] == '1') ? 0 : 1;
-    }();
-    return v != 0;
-}
-
 template <int K, int NG>
 static int dispatch_xs(GemvLaunch& L, cudaStream_t s) {
     if constexpr (NG == 1) {
-        if (use_v6() && L.m_x <= 8) {
+        if (L.m_x <= 8) {  // the lean v6 kernel; v5 serves the 16-row chunks of larger batches
             using G = G6<K, unit_bytes<K>()>;
             GemvLaunch L6 = L;
             int64_t mp = 0;
