@@ -509,12 +509,15 @@ static int run_c(const char* name) {
 int main() {
     uint32_t* dummy;
     cudaMalloc(&dummy, 4);
+    // profiles/r2_cta_shape.txt (CTAs per SM x warps) and r2_cta8.txt (8-warp CTAs)
     run_c<3, 16, 1>("compact 1x16");
+    run_c<3, 8, 1>("compact 1x8");
     run_c<3, 8, 2>("compact 2x8 (shipped shape)");
     run_c<3, 16, 2>("compact 2x16");
-    run_c<5, 16, 1>("compact 1x16");
     run_c<5, 8, 2>("compact 2x8");
-    run_c<8, 16, 1>("compact 1x16");
-    run_c<8, 12, 1>("compact 1x12 (shipped k=8)");
+    run_c<5, 16, 1>("compact 1x16");
+    run_c<5, 8, 1>("compact 1x8");
+    run_c<8, 12, 1>("compact 1x12");
+    run_c<8, 8, 1>("compact 1x8");
     return 0;
 }
