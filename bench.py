@@ -412,7 +412,7 @@ def run_ours(args):
                              "(dram_over_algorithmic x algorithmic)"},
         "clocks": clocks,
     }
-    if args.profile:
+    if args.profile or args.headline_only:
         if rank == 0:
             print(json.dumps(result))
         return
@@ -1032,6 +1032,8 @@ def main():
     ap.add_argument("--profile", action="store_true",
                     help="profiling run (under ncu): eager launches, skip detail/e2e/CPU legs")
     ap.add_argument("--no-decode", action="store_true", help="skip the C5 decode-step leg")
+    ap.add_argument("--headline-only", action="store_true",
+                    help="tuning runs: the timed graph only (no side legs, e2e or CPU baseline)")
     ap.add_argument("--nccl-gather", action="store_true",
                     help="N > 1: all-gather with NCCL after each GEMV instead of the fused epilogue stores")
     ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only (gloo, no GPU work)")

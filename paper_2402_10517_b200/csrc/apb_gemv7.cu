@@ -1133,6 +1133,11 @@ static int choose_cps(const Launch7& L) {
         return e ? std::atoi(e) : 0;
     }();
     if (forced == 1) return 1;
+    static const int cps1_k = [] {  // tuning: bit K set -> one CTA per SM at bit width K
+        const char* e = std::getenv("APB7_CPS1_K");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (cps1_k & (1 << K)) return 1;
     const bool fits2 = NB == 1 && Geo<K, NB, 2>::total(4, L.x_bufs * L.xs_bytes) <= kSmemLimit2;
     if (forced == 2) return fits2 ? 2 : 1;
     // measured: in a PDL chain of decode-sized launches (the bench step) two CTAs

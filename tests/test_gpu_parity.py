@@ -844,3 +844,50 @@ def test_dense_tcgen05_small_parent_and_rows(api):
         W = engine.dequantize(layer, k).astype(np.float64)
         y = engine.gemm(prep, X, engine.GemvConfig(bit_width=k, dense_threshold=16))
         assert ora.rel_err(y, X.astype(np.float64) @ W.T) < TOL, k
+
+
+_REPRO_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from oracle import oracle as ora
+from paper_2402_10517_b200 import AnyPrecisionLayer, engine, plan
+out = {{}}
+rng = np.random.default_rng(5)
+preps = []
+for i, (r, c) in enumerate([(2000, 3000), (1000, 3000), (3500, 3000)]):
+    codes, tables = ora.random_layer_arrays(np.random.default_rng(50 + i), r, c, 3, 8)
+    preps.append(engine.prepare(AnyPrecisionLayer(n_min=3, n_max=8, codes=codes, centroid_tables=tables, shape=(r, c))))
+x = torch.from_numpy(rng.standard_normal((1, 3000))).half().cuda()
+for k in (3, 5, 8):
+    p = plan.GemvPlan(preps, k, m=1, grouped=True, shared_x=True, y_fp16=False, pdl=True)
+    for xb in {{id(t): t for t in p.x}}.values():
+        xb[:, :3000].copy_(x)
+    for rep in range(3):
+        p.run()
+        torch.cuda.synchronize()
+        for j, y in enumerate(p.y):
+            out[f"k{{k}}_l{{j}}_r{{rep}}"] = y.cpu().numpy()
+np.savez({path!r}, **out)
+"""
+
+
+def test_gemv_grouped_bits_reproducible_across_processes(tmp_path):
+    # a grouped PDL launch (3 layers sharing x, more items than CTAs) gives the
+    # same bits run after run and in a second process (fixed partition and
+    # fixed fp32 reduction order, apb_gemv7.cu header)
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for run in ("a", "b"):
+        path = str(tmp_path / f"run_{run}.npz")
+        subprocess.run([sys.executable, "-c", _REPRO_SCRIPT.format(root=root, path=path)], check=True,
+                       cwd=root, timeout=600)
+        res[run] = np.load(path)
+    names = res["a"].files
+    assert len(names) == 27
+    for n in names:
+        assert np.array_equal(res["a"][n], res["b"][n]), n
+        base = n.rsplit("_r", 1)[0] + "_r0"
+        assert np.array_equal(res["b"][n], res["b"][base]), n
