@@ -289,8 +289,6 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
             }
             mbar_arrive(b_pe + 8 * s);
             const int sa = kb % kASlots;
-            if (kb >= kASlots) mbar_wait(b_ae + 8 * sa, ((kb / kASlots) - 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
             for (int w = 0; w < kWords; ++w) {
                 uint32_t W[8];
@@ -312,6 +310,10 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
                         }
                         v[4 * p + b / 2] = lo | (hi << 16);
                     }
+                if (w == 0) {  // decoded in registers while the MMA may still read the slot: wait only to store
+                    if (kb >= kASlots) mbar_wait(b_ae + 8 * sa, ((kb / kASlots) - 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                }
                 asm volatile(
                     "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
                         t_row + 32u * (uint32_t)sa + 16u * (uint32_t)w),
