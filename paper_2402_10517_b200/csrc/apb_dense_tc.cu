@@ -162,6 +162,25 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
+#ifdef APBD_TL
+// timing builds (tools/dense_tl.py): per-CTA globaltimer stamps / issuer wait cycles
+__device__ unsigned long long g_tld[8192 * 10];
+#define APBD_STAMP(i)                                                                                          \
+    do {                                                                                                       \
+        unsigned long long t_;                                                                                 \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                                \
+        g_tld[(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * 10 + (i)] = t_;              \
+    } while (0)
+#define APBD_SET(i, v) g_tld[(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * 10 + (i)] = (v)
+#else
+#define APBD_STAMP(i) \
+    do {              \
+    } while (0)
+#define APBD_SET(i, v) \
+    do {               \
+    } while (0)
+#endif
+
 template <int K, int BN>
 __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_constant__ DenseParams P) {
     using Y = Lay<BN, K>;
@@ -169,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (saddr(smem) != kSmemBase) __trap();  // the table base is an LDS immediate
+    if (threadIdx.x == 0) APBD_STAMP(0);
     const int64_t row0 = (int64_t)blockIdx.x * BM;
     const int n0 = blockIdx.y * BN;
     const uint32_t sX = saddr(smem + Y::kOffX), sP = saddr(smem + Y::kOffP);
@@ -205,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) APBD_STAMP(1);
     const int n_kb = P.n_kb;                  // this CTA's K blocks (split-K: blockIdx.z's share)
     const int kb0 = (int)blockIdx.z * n_kb;  // first global K block (even)
 
@@ -230,10 +251,23 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
     } else if (warp == 1) {
         // ============================ tcgen05.mma issuer ============================
         if (lane == 0) {
+#ifdef APBD_TL
+            long long wa = 0, wx = 0;
+#endif
             for (int kb = 0; kb < n_kb; ++kb) {
                 const int sa = kb % kASlots, sx = kb % kXStages;
+#ifdef APBD_TL
+                long long c0 = clock64();
+                mbar_wait(b_af + 8 * sa, (kb / kASlots) & 1);
+                long long c1 = clock64();
+                mbar_wait(b_xf + 8 * sx, (kb / kXStages) & 1);
+                wa += c1 - c0;
+                wx += clock64() - c1;
+                if (kb == 0) APBD_STAMP(2);
+#else
                 mbar_wait(b_af + 8 * sa, (kb / kASlots) & 1);
                 mbar_wait(b_xf + 8 * sx, (kb / kXStages) & 1);
+#endif
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint64_t dx = sw128_desc(sX + sx * BN * 128);
                 const uint32_t ta = tmem + Y::kColA + 32u * (uint32_t)sa;
@@ -244,6 +278,11 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
                 umma_commit(b_xe + 8 * sx);
             }
             umma_commit(b_d);  // accumulator complete
+            APBD_STAMP(3);
+#ifdef APBD_TL
+            APBD_SET(7, (unsigned long long)wa);
+            APBD_SET(8, (unsigned long long)wx);
+#endif
         }
     } else {
         // =================== decoders, then the epilogue ===================
@@ -270,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
             }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kDecWarps * 32) : "memory");  // table complete
+        if (warp == 2 && lane == 0) APBD_STAMP(6);
         const uint32_t rr = (uint32_t)r << 1;  // byte 0 of the table address
         // this warp's TMEM lane quarter; A slot columns of word h
         const uint32_t t_row = tmem + ((uint32_t)(32 * q4) << 16) + Y::kColA + 16u * (uint32_t)h;
@@ -328,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
         // ------------------------------------ epilogue ------------------------------------
         // the 4 warp groups (dw >> 2) split the BN accumulator columns
         mbar_wait(b_d, 0);
+        if (warp == 2 && lane == 0) APBD_STAMP(4);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         constexpr int kCols = BN / 4;                  // accumulator columns per warp group
         constexpr int kChunk = kCols < 32 ? kCols : 32;  // tcgen05.ld .x8 / .x16 / .x32
@@ -386,11 +427,25 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (threadIdx.x == 0) {
+        APBD_STAMP(5);
+#ifdef APBD_TL
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        APBD_SET(9, smid);
+#endif
+    }
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Y::kTmemCols));
     }
 }
+
+#ifdef APBD_TL
+extern "C" int apbd_read_timeline(unsigned long long* host, int n) {
+    return cudaMemcpyFromSymbol(host, g_tld, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 5;
+}
+#endif
 
 // Activations in the kernel's K order (one CTA per input row): fp16 rows copied,
 // or fp32 rows split into scaled (hi, lo) pairs at rows (2i, 2i+1) with 1 / scale
