@@ -45,6 +45,12 @@ namespace apbd {
 using apb::prmt;
 
 constexpr int BM = 128, BK = 64;
+#ifndef APBD_PAIR_SLOTS
+#define APBD_PAIR_SLOTS 8
+#endif
+#ifndef APBD_ONE256_SLOTS
+#define APBD_ONE256_SLOTS 4  // measured: 2 slots 0.345 ms, 4 slots 0.342, 8 slots 0.346 (11008x4096, M = 2048)
+#endif
 constexpr int kDecWarps = 16;  // (row quarter q, word h, K-block parity) -- 4 per SM sub-partition
 constexpr int kThreads = (2 + kDecWarps) * 32;
 constexpr int kSmemBase = 1024;  // sm_100 reserves the first 1 KB of the shared window
@@ -88,6 +94,7 @@ struct DenseParams {
     int64_t rows, ldy;
     int mx, m_out, n_kb, pairs;  // n_kb: K blocks per split (even)
     int splits;
+    int pair;  // CTA pairs (tm_x box = half the N tile per CTA)
 };
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -147,19 +154,50 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr_) {
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 // kind::f16 instruction descriptor: D f32, A/B f16, both K-major, N >> 3, M >> 4
-template <int BN>
-constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+template <int BN, int MM = BM>
+constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(MM >> 4) << 24);
 
-// A from tensor memory (the decoders' tcgen05.st), B from shared memory (TMA)
-template <int BN>
+// A from tensor memory (the decoders' tcgen05.st), B from shared memory (TMA).
+// PAIR: a CTA pair (cta_group::2, M = 256): A = both CTAs' TMEM lanes at the same
+// column, B = both CTAs' shared-memory halves (BN / 2 activation rows each) at
+// the same offset; issued by the pair's even CTA only.
+template <int BN, bool PAIR>
 __device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b), "n"(kIdesc<BN>), "r"(accumulate));
+    if constexpr (PAIR)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b), "n"(kIdesc<BN, 2 * BM>), "r"(accumulate));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b), "n"(kIdesc<BN>), "r"(accumulate));
 }
+// PAIR: the arrive lands on the barrier at the same offset in BOTH CTAs of the pair
+template <bool PAIR>
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+    if constexpr (PAIR)
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+            "h"((uint16_t)3)
+            : "memory");
+    else
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// wait for a phase completed by arrivals from the other CTA of a pair (cluster-scope acquire)
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+// the even CTA of the pair's copy of a shared-memory address (cluster window: rank bit 24)
+__device__ __forceinline__ uint32_t pair_leader(uint32_t a) { return a & 0xFEFFFFFFu; }
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 #ifdef APBD_TL
@@ -181,23 +219,34 @@ __device__ unsigned long long g_tld[8192 * 10];
     } while (0)
 #endif
 
-template <int K, int BN>
+template <int K, int BN, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_constant__ DenseParams P) {
     using Y = Lay<BN, K>;
-    constexpr int kXStages = Y::kXStages, kASlots = Y::kASlots, kPStages = Y::kPStages;
+    // PAIR: 4 A slots (TMEM 256 + 4 x 32 <= 512) -- a slot now waits on both CTAs' decoders
+    // PAIR: half-height activation stages, twice as many in the same bytes
+    constexpr int kXStages = PAIR ? 2 * Y::kXStages : Y::kXStages,
+                  kASlots = PAIR ? APBD_PAIR_SLOTS : (BN == 256 ? APBD_ONE256_SLOTS : Y::kASlots),
+                  kPStages = Y::kPStages;
+    constexpr int kXStage = (PAIR ? BN / 2 : BN) * 128;  // bytes of one activation stage in this CTA
+    static_assert(BN + 32 * kASlots <= Y::kTmemCols, "tensor memory budget");
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (saddr(smem) != kSmemBase) __trap();  // the table base is an LDS immediate
+    // the table base is an LDS immediate (+ the CTA's cluster rank at bit 24, carried in rr below)
+    if ((saddr(smem) & 0xFFFFFFu) != kSmemBase) __trap();
     if (threadIdx.x == 0) APBD_STAMP(0);
     const int64_t row0 = (int64_t)blockIdx.x * BM;
     const int n0 = blockIdx.y * BN;
+    uint32_t rank = 0;  // PAIR: rank in the CTA pair (clusters of 2 along the row tiles)
+    if constexpr (PAIR) asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const bool issuer_cta = !PAIR || rank == 0;
+    constexpr int kXRows = PAIR ? BN / 2 : BN;  // activation rows this CTA stages per K block
     const uint32_t sX = saddr(smem + Y::kOffX), sP = saddr(smem + Y::kOffP);
     const uint32_t bar = saddr(smem + Y::kOffB);
     // barriers (8 B each): x_full[8] x_empty[8] a_full[4] a_empty[4] p_full[8] p_empty[8] d_full
-    static_assert(kXStages <= 8 && kASlots <= 4 && kPStages <= 8, "barrier layout");
-    const uint32_t b_xf = bar, b_xe = bar + 64, b_af = bar + 128, b_ae = bar + 160, b_pf = bar + 192,
-                   b_pe = bar + 256, b_d = bar + 320;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Y::kOffB + 336);
+    static_assert(kXStages <= 8 && kASlots <= 8 && kPStages <= 8, "barrier layout");
+    const uint32_t b_xf = bar, b_xe = bar + 64, b_af = bar + 128, b_ae = bar + 192, b_pf = bar + 256,
+                   b_pe = bar + 320, b_d = bar + 384;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Y::kOffB + 400);
     constexpr int kPlaneBytes = Y::kPStride;  // one plane chunk stage: 16 B x 128 rows x K planes
 
     if (threadIdx.x == 0) {
@@ -206,23 +255,33 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
             mbar_init(b_xe + 8 * i, 1);
         }
         for (int i = 0; i < kASlots; ++i) {
-            mbar_init(b_af + 8 * i, (kASlots == 4 ? 4 : 8) * 32);  // the decoder warps of this K block
+            // the K block's decoder threads; PAIR: one arrive per decoder warp of both CTAs
+            mbar_init(b_af + 8 * i, PAIR ? 2 * (kASlots >= 4 ? 4 : 8) : (kASlots >= 4 ? 4 : 8) * 32);
             mbar_init(b_ae + 8 * i, 1);
         }
         for (int i = 0; i < kPStages; ++i) {
             mbar_init(b_pf + 8 * i, 1);
-            mbar_init(b_pe + 8 * i, (kASlots == 4 ? 8 : kDecWarps) * 32);  // decoders of its two K blocks
+            mbar_init(b_pe + 8 * i, (kASlots >= 4 ? 8 : kDecWarps) * 32);  // decoders of its two K blocks
         }
         mbar_init(b_d, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {  // D[128 lanes][BN] fp32 + the decoded A slots
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tmem_slot)),
-                     "n"(Y::kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tmem_slot)),
+                         "n"(Y::kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tmem_slot)),
+                         "n"(Y::kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    if constexpr (PAIR)
+        cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA arrive / TMA
+    else
+        __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) APBD_STAMP(1);
@@ -244,13 +303,24 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
             for (int kb = 0; kb < n_kb; ++kb) {
                 const int s = kb % kXStages;
                 if (kb >= kXStages) mbar_wait(b_xe + 8 * s, ((kb / kXStages) - 1) & 1);
-                mbar_expect_tx(b_xf + 8 * s, BN * 128);
-                tma2(sX + s * BN * 128, &P.tm_x, (kb0 + kb) * BK, n0, b_xf + 8 * s);
+                if constexpr (PAIR) {
+                    // each CTA stages its half of the tile; both halves complete on the even
+                    // CTA's barrier, which expects the whole tile
+                    if (rank == 0) mbar_expect_tx(b_xf + 8 * s, BN * 128);
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                            sX + s * kXStage),
+                        "l"(&P.tm_x), "r"((kb0 + kb) * BK), "r"(n0 + (int)rank * kXRows), "r"(pair_leader(b_xf + 8 * s))
+                        : "memory");
+                } else {
+                    mbar_expect_tx(b_xf + 8 * s, BN * 128);
+                    tma2(sX + s * kXStage, &P.tm_x, (kb0 + kb) * BK, n0, b_xf + 8 * s);
+                }
             }
         }
     } else if (warp == 1) {
         // ============================ tcgen05.mma issuer ============================
-        if (lane == 0) {
+        if (lane == 0 && issuer_cta) {
 #ifdef APBD_TL
             long long wa = 0, wx = 0;
 #endif
@@ -265,19 +335,22 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
                 wx += clock64() - c1;
                 if (kb == 0) APBD_STAMP(2);
 #else
-                mbar_wait(b_af + 8 * sa, (kb / kASlots) & 1);
+                if constexpr (PAIR)
+                    mbar_wait_cluster(b_af + 8 * sa, (kb / kASlots) & 1);
+                else
+                    mbar_wait(b_af + 8 * sa, (kb / kASlots) & 1);
                 mbar_wait(b_xf + 8 * sx, (kb / kXStages) & 1);
 #endif
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint64_t dx = sw128_desc(sX + sx * BN * 128);
+                const uint64_t dx = sw128_desc(sX + sx * kXStage);
                 const uint32_t ta = tmem + Y::kColA + 32u * (uint32_t)sa;
 #pragma unroll
                 for (int ks = 0; ks < BK / 16; ++ks)  // K = 16 per MMA: 8 TMEM columns of A, +32 B of B's swizzle atom
-                    umma_f16_ts<BN>(tmem, ta + 8u * (uint32_t)ks, dx + 2 * ks, (kb | ks) != 0);
-                umma_commit(b_ae + 8 * sa);  // the decoded tile and the x tile may be overwritten
-                umma_commit(b_xe + 8 * sx);
+                    umma_f16_ts<BN, PAIR>(tmem, ta + 8u * (uint32_t)ks, dx + 2 * ks, (kb | ks) != 0);
+                umma_commit<PAIR>(b_ae + 8 * sa);  // the decoded tile and the x tile may be overwritten
+                umma_commit<PAIR>(b_xe + 8 * sx);
             }
-            umma_commit(b_d);  // accumulator complete
+            umma_commit<PAIR>(b_d);  // accumulator complete
             APBD_STAMP(3);
 #ifdef APBD_TL
             APBD_SET(7, (unsigned long long)wa);
@@ -290,8 +363,8 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
         // warp may write / read).  2 A slots: lane word h of every K block with parity
         // par; 4 A slots: both lane words of every K block kb = ph (mod 4)
         const int dw = warp - 2, q4 = warp & 3;
-        const int h = kASlots == 4 ? 0 : (dw >> 2) & 1, par = kASlots == 4 ? dw >> 2 : dw >> 3;
-        constexpr int kWords = kASlots == 4 ? 2 : 1;
+        const int h = kASlots >= 4 ? 0 : (dw >> 2) & 1, par = kASlots >= 4 ? dw >> 2 : dw >> 3;
+        constexpr int kWords = kASlots >= 4 ? 2 : 1;
         const int r = 32 * q4 + lane;
         const int64_t grow = row0 + r;
         // this row's centroid table: u32 [entry][128 rows] (k <= 7), u16 (k = 8); the
@@ -310,10 +383,12 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kDecWarps * 32) : "memory");  // table complete
         if (warp == 2 && lane == 0) APBD_STAMP(6);
-        const uint32_t rr = (uint32_t)r << 1;  // byte 0 of the table address
+        // byte 0 of the table address; bytes 2-3 carry this CTA's shared-window rank bit
+        // (bit 24 of the address after the u32 path's << 1), kept by the PRMT below
+        const uint32_t rr = ((uint32_t)r << 1) | ((saddr(smem) & 0xFF000000u) >> (K <= 7 ? 1 : 0));
         // this warp's TMEM lane quarter; A slot columns of word h
         const uint32_t t_row = tmem + ((uint32_t)(32 * q4) << 16) + Y::kColA + 16u * (uint32_t)h;
-        for (int kb = par; kb < n_kb; kb += (kASlots == 4 ? 4 : 2)) {
+        for (int kb = par; kb < n_kb; kb += (kASlots >= 4 ? 4 : 2)) {
             // this row's lane word(s) of K block kb: plane chunk stage kb / 2, words 2 (kb & 1) + h (+1)
             const int ps = kb >> 1, s = ps % kPStages;
             mbar_wait(b_pf + 8 * s, (ps / kPStages) & 1);
@@ -363,7 +438,13 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(b_af + 8 * sa);
+            if constexpr (PAIR) {  // the even CTA issues the pair's MMA: one cluster-scope arrive per warp
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(pair_leader(b_af + 8 * sa))
+                                 : "memory");
+            } else
+                mbar_arrive(b_af + 8 * sa);
         }
         // ------------------------------------ epilogue ------------------------------------
         // the 4 warp groups (dw >> 2) split the BN accumulator columns
@@ -426,7 +507,10 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    if constexpr (PAIR)
+        cluster_sync_all();  // no CTA of the pair leaves while the other may still signal it
+    else
+        __syncthreads();
     if (threadIdx.x == 0) {
         APBD_STAMP(5);
 #ifdef APBD_TL
@@ -437,7 +521,10 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tc_kernel(const __grid_cons
     }
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Y::kTmemCols));
+        if constexpr (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Y::kTmemCols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Y::kTmemCols));
     }
 }
 
@@ -522,14 +609,27 @@ static EncodeTiledFn encode_fn() {
     return fn;
 }
 
-template <int K, int BN>
+template <int K, int BN, bool PAIR>
 static int launch_bn(DenseParams& P, int64_t rows, cudaStream_t s) {
     static std::atomic<unsigned long long> configured{0};
     static_assert(Lay<BN, K>::kBytes <= 227 * 1024, "shared memory budget");
-    if (!apb::ensure_smem_optin(dense_tc_kernel<K, BN>, Lay<BN, K>::kBytes, configured)) return APB_ERR_CUDA;
-    const dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((P.mx + BN - 1) / BN), (unsigned)P.splits);
-    dense_tc_kernel<K, BN><<<grid, kThreads, Lay<BN, K>::kBytes, s>>>(P);
-    if (cudaGetLastError() != cudaSuccess) return APB_ERR_CUDA;
+    auto kern = dense_tc_kernel<K, BN, PAIR>;
+    if (!apb::ensure_smem_optin(kern, Lay<BN, K>::kBytes, configured)) return APB_ERR_CUDA;
+    int64_t row_tiles = (rows + BM - 1) / BM;
+    if (PAIR) row_tiles = (row_tiles + 1) / 2 * 2;  // whole CTA pairs (an all-padding tile reads zeros, stores nothing)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)row_tiles, (unsigned)((P.mx + BN - 1) / BN), (unsigned)P.splits);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Lay<BN, K>::kBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = PAIR ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, kern, P) != cudaSuccess) return APB_ERR_CUDA;
     if (P.splits > 1) {
         const int64_t n = (int64_t)P.m_out * rows;
         split_sum_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P.ws, P.splits, P.mx, rows, P.pairs, P.inv, P.y,
@@ -541,14 +641,27 @@ static int launch_bn(DenseParams& P, int64_t rows, cudaStream_t s) {
 // decoded weight tile then feeds twice the MMA work); small batches stage only
 // the rows they have (the activation tile is shared-memory traffic per K block)
 static int pick_bn(int64_t mx) { return mx > 128 ? 256 : (mx > 64 ? 128 : (mx > 32 ? 64 : 32)); }
+// CTA pairs (cta_group::2, M = 256) for the 256-wide N tile without split-K:
+// each SM of a pair stages and reads half of every activation tile.  Opt-in
+// (APB_DENSE_PAIR=1): correct (tests) but measured ~15 % slower than one CTA
+// per tile -- every K block then waits for both CTAs' decoders
+// (profiles/r2_dense_overlap.md).
+static bool pair_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("APB_DENSE_PAIR");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 template <int K>
 static int launch(DenseParams& P, int64_t rows, cudaStream_t s) {
     switch (pick_bn(P.mx)) {
-        case 32: return launch_bn<K, 32>(P, rows, s);
-        case 64: return launch_bn<K, 64>(P, rows, s);
-        case 128: return launch_bn<K, 128>(P, rows, s);
+        case 32: return launch_bn<K, 32, false>(P, rows, s);
+        case 64: return launch_bn<K, 64, false>(P, rows, s);
+        case 128: return launch_bn<K, 128, false>(P, rows, s);
     }
-    return launch_bn<K, 256>(P, rows, s);
+    if (P.pair) return launch_bn<K, 256, true>(P, rows, s);
+    return launch_bn<K, 256, false>(P, rows, s);
 }
 
 }  // namespace apbd
@@ -604,9 +717,21 @@ extern "C" int apb_gemm_dense_tc(const uint8_t* planes, int n_max, int64_t rows,
     if (!enc) return APB_ERR_CUDA;
     DenseParams P = {};
     {
+        int sms = 148, dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int bn = pick_bn(mx);
+        const int64_t tiles = ((rows + BM - 1) / BM) * ((mx + bn - 1) / bn);
+        int sp = choose_splits(tiles, (int)(padded_cols / BK), sms);
+        if (sp > 1 && (!ws || ws_bytes < (int64_t)sp * mx * rows * 4)) sp = 1;  // no workspace: one pass
+        P.splits = sp;
+        P.ws = ws;
+        P.n_kb = (int)(padded_cols / BK) / sp;
+    }
+    P.pair = pick_bn(mx) == 256 && P.splits == 1 && rows > BM && pair_enabled() ? 1 : 0;
+    {
         const cuuint64_t dims[2] = {(cuuint64_t)padded_cols, (cuuint64_t)mx};
         const cuuint64_t strides[1] = {(cuuint64_t)padded_cols * 2};
-        const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)pick_bn(mx)}, es[2] = {1, 1};  // N tile (launch)
+        const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)(pick_bn(mx) >> P.pair)}, es[2] = {1, 1};  // N tile / CTA
         if (enc(&P.tm_x, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)xp, dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -630,17 +755,6 @@ extern "C" int apb_gemm_dense_tc(const uint8_t* planes, int n_max, int64_t rows,
     P.mx = (int)mx;
     P.m_out = (int)m_out;
     P.pairs = pairs ? 1 : 0;
-    {
-        int sms = 148, dev = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int bn = pick_bn(mx);
-        const int64_t tiles = ((rows + BM - 1) / BM) * ((mx + bn - 1) / bn);
-        int sp = choose_splits(tiles, (int)(padded_cols / BK), sms);
-        if (sp > 1 && (!ws || ws_bytes < (int64_t)sp * mx * rows * 4)) sp = 1;  // no workspace: one pass
-        P.splits = sp;
-        P.ws = ws;
-        P.n_kb = (int)(padded_cols / BK) / sp;
-    }
     cudaStream_t s = (cudaStream_t)stream;
     switch (k) {
         case 2: return launch<2>(P, rows, s);

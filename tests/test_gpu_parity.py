@@ -891,3 +891,39 @@ def test_gemv_grouped_bits_reproducible_across_processes(tmp_path):
         assert np.array_equal(res["a"][n], res["b"][n]), n
         base = n.rsplit("_r", 1)[0] + "_r0"
         assert np.array_equal(res["b"][n], res["b"][base]), n
+
+
+_PAIR_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from oracle import oracle as ora
+from paper_2402_10517_b200 import AnyPrecisionLayer, engine
+out = {{}}
+for rows, cols, m, k in ((300, 3000, 300, 4), (4096, 4096, 512, 3), (1000, 2048, 257, 8)):
+    codes, tables = ora.random_layer_arrays(np.random.default_rng(rows + m), rows, cols, 3, 8)
+    layer = AnyPrecisionLayer(n_min=3, n_max=8, codes=codes, centroid_tables=tables, shape=(rows, cols))
+    prep = engine.prepare(layer)
+    x = np.random.default_rng(m).standard_normal((m, cols)).astype(np.float32)
+    out[f"{{rows}}_{{m}}_{{k}}"] = engine.gemm(prep, x, engine.GemvConfig(bit_width=k))
+    W = engine.dequantize(layer, k).astype(np.float64)
+    out[f"{{rows}}_{{m}}_{{k}}_ref"] = x.astype(np.float64) @ W.T
+np.savez({path!r}, **out)
+"""
+
+
+def test_dense_cta_pair_path_vs_oracle(tmp_path):
+    # the opt-in CTA-pair (cta_group::2) dense kernel (APB_DENSE_PAIR=1) against
+    # the fp64 product of the reference dequantisation at the 1e-5 bar, M > 128
+    # (the 256-wide pair tile), an odd number of 128-row tiles (an all-padding CTA)
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = str(tmp_path / "pair.npz")
+    subprocess.run([sys.executable, "-c", _PAIR_SCRIPT.format(root=root, path=path)],
+                   env=dict(os.environ, APB_DENSE_PAIR="1"), check=True, cwd=root, timeout=600)
+    r = np.load(path)
+    names = [n for n in r.files if not n.endswith("_ref")]
+    assert len(names) == 3
+    for n in names:
+        assert ora.rel_err(r[n], r[n + "_ref"]) < TOL, (n, ora.rel_err(r[n], r[n + "_ref"]))
