@@ -343,10 +343,13 @@ def run_ours(args):
         else:
             for sp in fused:
                 sp._spin = 1 << 26
+    # NVTX ranges name the bench phases on profiler timelines (SURVEY §5 tracing)
+    nvtx = torch.cuda.nvtx.range
     # warm-up (also configures kernel attributes before capture)
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
+    with nvtx("bench/warmup"):
+        for _ in range(max(3, args.warmup)):
+            step()
+        torch.cuda.synchronize()
     graph = None
     try:
         if args.profile:
@@ -365,7 +368,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk, nvtx(f"bench/timed {args.steps} steps"):
         start.record()
         for _ in range(args.steps):
             if graph is not None:
@@ -416,30 +419,34 @@ def run_ours(args):
         if rank == 0:
             print(json.dumps(result))
         return
+    def leg(name, fn, *a):
+        with nvtx(f"bench/{name}"):
+            result[name] = fn(*a)
+
     if world == 1:
-        result["per_gemv_us"] = per_gemv_detail(torch, plan, copies, peak)
-        result["fp16_cublas_gemv"] = fp16_gemv_detail(torch, result["per_gemv_us"])
-        result["grouped_all7_GBps"] = grouped_all7(torch, plan, copies)
-        result["packer"] = packer_detail(torch)
-        result["small_batch_C3"] = small_batch_detail(torch, plan, copies)
-        result["shard70b_C4_per_rank"] = shard70b_detail(torch, plan)
+        leg("per_gemv_us", per_gemv_detail, torch, plan, copies, peak)
+        leg("fp16_cublas_gemv", fp16_gemv_detail, torch, result["per_gemv_us"])
+        leg("grouped_all7_GBps", grouped_all7, torch, plan, copies)
+        leg("packer", packer_detail, torch)
+        leg("small_batch_C3", small_batch_detail, torch, plan, copies)
+        leg("shard70b_C4_per_rank", shard70b_detail, torch, plan)
     if world > 1:
         try:
             result["shard70b_C4"] = shard70b_multi(torch, plan, world, rank, share)
         except Exception as e:  # never lose the headline to the side leg
             result["shard70b_C4"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if world == 1 and not args.no_decode:
-        result["decode_step"] = run_decode(torch)
-        result["quantizer"] = run_quantizer(torch)
-        result["prefill_dense"] = run_prefill(torch, copies[0])
+        leg("decode_step", run_decode, torch)
+        leg("quantizer", run_quantizer, torch)
+        leg("prefill_dense", run_prefill, torch, copies[0])
     if rank == 0:
         if world == 1:
-            result["e2e"] = run_e2e_step(torch, plans, world)
-            result["e2e_per_call"] = run_e2e(torch, copies[0], world)
+            leg("e2e", run_e2e_step, torch, plans, world)
+            leg("e2e_per_call", run_e2e, torch, copies[0], world)
         else:
-            result["e2e"] = run_e2e(torch, copies[0], world)
+            leg("e2e", run_e2e, torch, copies[0], world)
         if world == 1:
-            result["cpu_baseline"] = cpu_baseline()
+            leg("cpu_baseline", cpu_baseline)
         print(json.dumps(result))
     if world > 1:
         dist.destroy_process_group()
