@@ -927,3 +927,52 @@ def test_dense_cta_pair_path_vs_oracle(tmp_path):
     assert len(names) == 3
     for n in names:
         assert ora.rel_err(r[n], r[n + "_ref"]) < TOL, (n, ora.rel_err(r[n], r[n + "_ref"]))
+
+
+# ---- reference edge cases (test_engine.py:141-163, 247-253) ----------------------------
+
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
+def test_zero_activations_give_exact_zero(api, k):
+    # test_engine.py:141-145: zero x -> y exactly 0 on every path (quantized GEMV,
+    # small batch, tcgen05 dense), fp32 and fp16 activations
+    _, _, engine, _ = api
+    prep = engine.prepare(_random_layer(api, 4, 8, 1024, 2, 5))
+    for fp16 in (False, True):
+        assert not engine.gemv(prep, np.zeros(1024), engine.GemvConfig(bit_width=k, activations_fp16=fp16)).any()
+        for m in (3, 40):
+            y = engine.gemm(prep, np.zeros((m, 1024)), engine.GemvConfig(bit_width=k, activations_fp16=fp16))
+            assert y.shape == (m, 8) and not y.any(), (m, fp16)
+
+
+@pytest.mark.parametrize("rows,cols,n_max", [(4, 1024, 4), (1, 1, 8), (3, 5, 3), (17, 1025, 8)])
+def test_tiny_and_ragged_layers_vs_oracle(api, rows, cols, n_max):
+    # test_engine.py:157-163 (4 x 1024 full-width tiny layer) plus a 1 x 1 layer, a
+    # sub-tile ragged one and one a row / column past a tile: gemv and gemm
+    # (quantized and dense paths) against the C oracle at the 1e-5 bar
+    _, _, engine, _ = api
+    layer = _random_layer(api, rows * 7 + cols, rows, cols, 2, n_max)
+    prep = engine.prepare(layer)
+    planes = prep.planes.cpu().numpy()
+    rng = np.random.default_rng(cols)
+    for k in range(2, n_max + 1):
+        t = layer.centroid_tables[k]
+        x = rng.standard_normal(cols)
+        want = ora.gemm(planes, cols, k, t, ora.prep_x(x, cols, False), nthreads=4)
+        assert ora.rel_err(engine.gemv(prep, x, engine.GemvConfig(bit_width=k)), want) < TOL, k
+        X = rng.standard_normal((20, cols))
+        W = engine.dequantize(layer, k).astype(np.float64)
+        y = engine.gemm(prep, X, engine.GemvConfig(bit_width=k))  # M = 20 > 16: dense path
+        assert ora.rel_err(y, X @ W.T) < TOL, k
+        y4 = engine.gemm(prep, X[:4], engine.GemvConfig(bit_width=k))  # quantized small batch
+        assert ora.rel_err(y4, X[:4] @ W.T) < TOL, k
+
+
+def test_gemm_m1_equals_gemv(api):
+    # test_engine.py:247-253: a one-row GEMM is the GEMV (here bit-identical)
+    _, _, engine, _ = api
+    prep = engine.prepare(_random_layer(api, 13, 6, 1024, 2, 5))
+    x = np.random.default_rng(13).standard_normal((1, 1024))
+    for k in (2, 3, 4, 5):
+        y = engine.gemm(prep, x, engine.GemvConfig(bit_width=k))
+        yv = engine.gemv(prep, x[0], engine.GemvConfig(bit_width=k))
+        assert np.array_equal(y[0], yv), k
