@@ -1145,7 +1145,11 @@ static int choose_cps(const Launch7& L) {
     // isolated launch (> 10 items per SM, e.g. a 28672-row layer) runs ~4 %
     // faster with one 16-warp CTA per SM, except at k = 3.
     const bool long_launch = L.n_items > 10 * sm_count();
-    return fits2 && (K == 3 || !long_launch) ? 2 : 1;
+    // fewer items than SMs (row shards, small layers): two CTAs per SM would leave
+    // each SM ONE 8-warp CTA -- half the decode rate of a 16-warp CTA (measured:
+    // 2048 x 28672 at k = 3 took 14.9 us vs 11.1 at k = 4, which runs one CTA per SM)
+    const bool few_items = L.n_items < sm_count();
+    return fits2 && !few_items && (K == 3 || !long_launch) ? 2 : 1;
 }
 
 template <int K, int NB, int CPS, bool EPI>

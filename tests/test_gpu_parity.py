@@ -516,7 +516,8 @@ def test_norm_plan_rejects_split_activations(api):
 
 
 def test_grouped_equals_single(api):
-    # the grouped launch (one kernel for several layers) is bit-identical
+    # the grouped launch (one kernel for several layers) gives each layer's own
+    # result (random activations; the round-1 version compared all-zero outputs)
     import torch
 
     from paper_2402_10517_b200 import plan
@@ -524,16 +525,22 @@ def test_grouped_equals_single(api):
     _, _, engine, _ = api
     shapes = [(4096, 4096), (1100, 4096), (4096, 11008), (17, 300)]
     preps = [engine.prepare(_random_layer(api, 100 + i, r, c)) for i, (r, c) in enumerate(shapes)]
+    g = torch.Generator(device="cuda").manual_seed(11)
     for k in (3, 4, 6, 8):
         p = plan.GemvPlan(preps, k, m=1, grouped=True)
         q = plan.GemvPlan(preps, k, m=1, grouped=False)
-        for xa, xb in zip(p.x, q.x):
+        for (r, c), xa, xb in zip(shapes, p.x, q.x):
+            xa[:, :c].copy_(torch.randn(1, c, device="cuda", generator=g).half())
             xb.copy_(xa)
         p.run()
         q.run()
         torch.cuda.synchronize()
-        for ya, yb in zip(p.y, q.y):
-            assert torch.equal(ya, yb), k
+        for (r, c), ya, yb in zip(shapes, p.y, q.y):
+            # the same products; the fp32 sums are split by warp group along each CTA's
+            # item sequence, which the partition of the grouped launch shifts: equal
+            # within fp32 reassociation (each launch shape itself is bit-reproducible)
+            assert ya.abs().max() > 0
+            assert float((ya - yb).norm() / yb.norm()) < 1e-6, (k, r)
 
 
 def test_large_shape_properties(api):
@@ -594,8 +601,11 @@ def test_step_plan_host_roundtrip(api):
     x1 = sp.x_host[1][0, :3000].clone()
     cfg3 = engine.GemvConfig(bit_width=3, activations_fp16=True)
     cfg8 = engine.GemvConfig(bit_width=8, activations_fp16=True)
-    assert torch.equal(y[0][0], engine.gemv(preps[0], x0, cfg3))
-    assert torch.equal(y[1][0], engine.gemv(preps[1], x0, cfg3))
+    # grouped launch vs each layer alone: the same products, fp32 sums split by warp
+    # group along a different CTA partition -- equal within fp32 reassociation
+    for j in (0, 1):
+        yj = engine.gemv(preps[j], x0, cfg3)
+        assert float((y[j][0] - yj).norm() / yj.norm()) < 1e-6, j
     assert torch.equal(y[2][0], engine.gemv(preps[2], x1, cfg8))
     # the copies are graph nodes: new host inputs are read on every replay, and
     # the copy-less graph (host copies issued around it) gives the same bits
@@ -604,7 +614,8 @@ def test_step_plan_host_roundtrip(api):
     y2 = [t.clone() for t in sp.run_host()]
     x0 = sp.x_host[0][0, :4096].clone()
     x1 = sp.x_host[1][0, :3000].clone()
-    assert torch.equal(y2[0][0], engine.gemv(preps[0], x0, cfg3))
+    y20 = engine.gemv(preps[0], x0, cfg3)
+    assert float((y2[0][0] - y20).norm() / y20.norm()) < 1e-6
     assert torch.equal(y2[2][0], engine.gemv(preps[2], x1, cfg8))
     sp.capture(host_copies=False)
     y3 = [t.clone() for t in sp.run_host()]
